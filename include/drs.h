@@ -1,0 +1,134 @@
+/* drs.h -- C ABI of libdrs.so, the B200 (sm_100a) kernels behind the
+ * DRiffusion draft-and-refine sampler (package paper_2603_25872_b200).
+ *
+ * Every entry point takes plain pointers/sizes and a cudaStream_t (passed as
+ * void*), launches asynchronously on that stream, never allocates, never
+ * synchronises, and returns an int status (DRS_OK or one of the codes below).
+ * Argument validation happens on the host before any launch, so a non-zero
+ * status means nothing was enqueued.  Device-side failures that can only be
+ * detected while running (a ziggurat tail needing more lookahead than the
+ * window holds) are reported through the caller's `err` word, which the host
+ * wrapper inspects after the run (see paper_2603_25872_b200/_lib.py).
+ *
+ * The reference (skipdiff, /root/reference/pkg/src/skipdiff) has no FFI: its
+ * boundary is Python.  Each function below replaces one reference routine;
+ * the citation says which.  The ctypes binding a skipdiff maintainer would add
+ * is in INTEGRATION.md.
+ */
+#ifndef DRS_H_
+#define DRS_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1:1 with skipdiff/errors.py (+ ValueError/TypeError) -- */
+#define DRS_OK                       0
+#define DRS_ERR_VALUE                1  /* ValueError (bad argument, z missing)        */
+#define DRS_ERR_TIMESTEP_OUT_OF_RANGE 2 /* errors.py:12  TimestepOutOfRange           */
+#define DRS_ERR_INVALID_SKIP         3  /* errors.py:24  InvalidSkip                  */
+#define DRS_ERR_VARIANCE_TOO_LARGE   4  /* errors.py:28  VarianceTooLarge             */
+#define DRS_ERR_DIMENSION_MISMATCH   5  /* errors.py:16  DimensionMismatch            */
+#define DRS_ERR_INVALID_PLAN         6  /* errors.py:40  InvalidPlanParams            */
+#define DRS_ERR_CUDA                 7  /* launch failure (cudaGetLastError != 0)     */
+#define DRS_ERR_NOISE_WINDOW         8  /* device: ziggurat tail exceeded lookahead   */
+
+/* ---- noise generators ---------------------------------------------------- */
+#define DRS_GEN_PCG64 0  /* numpy PCG64 (XSL-RR 128/64): skipdiff rng.py:32        */
+#define DRS_GEN_SFC64 1  /* numpy SFC64 seeded by the same SeedSequence key        */
+
+/* One counter-based stream key = the entropy tuple numpy's SeedSequence sees.
+ *   skipdiff rng.py:32      -> (0x7A9C, seed & 0xFFFFFFFFFFFF, t, role)
+ *   skipdiff denoiser.py:144 -> (0x51DE, seed & 0xFFFFFFFF, t)
+ * vals[0..n_vals) are non-negative integers (each becomes 1..2 little-endian
+ * uint32 words, 0 -> [0]).  If seed_slot >= 0, vals[1] is replaced on device
+ * by seeds[seed_slot] & seed_mask, so a captured CUDA graph can be replayed
+ * for a new seed by rewriting one device word. */
+typedef struct drs_key {
+  int64_t vals[4];
+  int32_t n_vals;
+  int32_t seed_slot;
+  uint64_t seed_mask;
+} drs_key;
+
+/* Fill out[s*ld + 0..n) with the first n standard normals of stream keys[s],
+ * bit-identical to numpy `Generator(BitGen(SeedSequence(key))).standard_normal(n)`
+ * (numpy random_standard_normal ziggurat; glibc log1p/exp on the slow paths).
+ * keys and seeds are DEVICE pointers.  Replaces rng.py:27-33 derive_noise and
+ * denoiser.py:139-145 state_independent_eps.  One CTA per stream. */
+int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const uint64_t* seeds,
+                   int64_t n, double* out, int64_t ld, int* err, void* stream);
+
+/* ---- skip transitions (K2/K3) -------------------------------------------- */
+#define DRS_FAMILY_DDIM 0     /* ddim_skip                                   */
+#define DRS_FAMILY_DDPM 1     /* ddpm_skip_sample(.., predicted_x0(eps), z)  */
+#define DRS_FAMILY_DDPM_X0 2  /* ddpm_skip_sample with x0_hat given in eps   */
+#define DRS_FAMILY_PRED_X0 3  /* predicted_x0: (x - c0 eps)/c1               */
+#define DRS_FAMILY_EULER 4    /* euler_skip: x + c0 v   (transitions.py:188) */
+#define DRS_SRC_X   0   /* op input = op.x (a state vector in HBM)             */
+#define DRS_SRC_CUR 1   /* op input = result of the previous op (register)    */
+#define DRS_SRC_ANCHOR 2 /* op input = result saved by the last SAVE_ANCHOR op */
+#define DRS_OP_SAVE_ANCHOR 1
+
+/* One elementwise skip update x_{t-k} = F(x_t, eps[, z]) with host-computed
+ * fp64 coefficients (expression order of the reference, no FMA contraction):
+ *  DDIM (transitions.py:155-179):
+ *    c = {sqrt(1-ab_t), sqrt(ab_t), sqrt(ab_s), sqrt(1-ab_s-sigma**2), sigma, -}
+ *    x0 = (x - c0*eps)/c1 ; out = c2*x0 + c3*eps ; if noisy: out = out + c4*z
+ *  DDPM (sequential.py:51-54 + transitions.py:105-134):
+ *    c = {sqrt(1-ab_t), sqrt(ab_t), sqrt(r)*(1-ab_s), sqrt(ab_s)*(1-r), 1-ab_t, sqrt(var)}
+ *    x0 = (x - c0*eps)/c1 ; out = (c2*x + c3*x0)/c4 ; if noisy: out = out + c5*z
+ * eps is fp64 (eps_f32 == 0) or fp32 (eps_f32 == 1, upcast exactly). */
+typedef struct drs_op {
+  double c[6];
+  int32_t family;
+  int32_t noisy;
+  int32_t src;
+  int32_t flags;
+  int32_t eps_f32;
+  int32_t pad;
+  const double* x;
+  const void* eps;
+  const double* z;
+  double* out;
+  double* out2;
+} drs_op;
+
+/* Run ops[0..n_ops) (a DEVICE array) in order for every element j < D.
+ * Intermediate states stay in registers; each op writes out/out2 if set.
+ * Replaces ddim_skip / ddpm_skip_sample calls of parallel.py:256-306 and
+ * sequential.py:68-74,106-111: a draft fan-out, a refine chain, or a refine
+ * chain fused with the next block's drafts, in one launch. n_ops <= 64. */
+int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* stream);
+
+/* ---- toy eps oracle (K9) ------------------------------------------------- */
+/* Gaussian-mixture eps (denoiser.py:73-107) for rows r < n_rows:
+ *   x = xs[r] (fp64, D), t = ts[r] (DEVICE int32), abar = alpha_bar[t]
+ *   eps[r] = -sqrt(1-abar) * sum_i resp_i(x) (sqrt(abar) m_i - x)/s_i,
+ *   s_i = abar v_i + 1-abar.  means: n_comp x D fp64, logw/var: n_comp fp64.
+ * xs / out are DEVICE arrays of n_rows pointers.  n_comp <= 8. */
+int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows, int64_t D,
+               const double* alpha_bar, int T, const double* means, const double* log_w,
+               const double* var, int n_comp, double* const* out, int* err, void* stream);
+
+/* Copy rows: out[r][0..D) = src[r][0..D) (DEVICE pointer arrays). */
+int drs_copy_rows(const double* const* src, double* const* out, int n_rows, int64_t D,
+                  void* stream);
+
+/* Busy-wait `n_ctas` CTAs for `us` microseconds each (concurrently): the
+ * device analogue of the Latency wrapper's sleep (denoiser.py:204-209,258-263). */
+int drs_spin(double us, int n_ctas, void* stream);
+
+/* Host-side ports used by the device kernels, exported for the CPU tests. */
+double drs_host_log1p(double x);
+double drs_host_exp(double x);
+/* Host restatement of SeedSequence(key).generate_state(n_words32, uint32). */
+int drs_host_seedseq(const drs_key* key, uint64_t seed, uint32_t* out, int n_words32);
+
+int drs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRS_H_ */

@@ -1,0 +1,67 @@
+"""Build libdrs.so (the sm_100a kernels + C ABI) in-tree with nvcc.
+
+    python -m paper_2603_25872_b200._build [--force] [-v]
+
+Every translation unit is compiled with contraction disabled (--fmad=false on
+device, -ffp-contract=off on the host side) because the sampler kernels are
+bit-exact restatements of numpy/glibc arithmetic; the few fused
+multiply-adds that ARE part of the reference arithmetic (glibc's FMA builds
+of log1p/exp) are written as explicit fma() calls.
+"""
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+BUILD = os.path.join(ROOT, "build", "drs")
+LIB = os.path.join(PKG, "libdrs.so")
+
+SOURCES = ["noise.cu", "chain.cu", "gm_eps.cu", "misc.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
+    return cand if os.path.exists(cand) else "nvcc"
+
+
+def _flags():
+    return ARCH + [
+        "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+        "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+        "-I", INCLUDE, "-I", CSRC,
+    ]
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "drs.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    newest_dep = max(os.path.getmtime(p) for p in _deps())
+    objs = []
+    for src in SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        objs.append(o)
+        if not force and os.path.exists(o) and os.path.getmtime(o) >= newest_dep:
+            continue
+        cmd = [nvcc()] + _flags() + ["-c", s, "-o", o]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,131 @@
+"""ctypes binding of libdrs.so (include/drs.h).
+
+The product path has no CPU fallback: importing a compute entry point without
+the built library, or calling one without a CUDA device, raises
+`NativeLibraryMissing` / `RuntimeError` immediately.
+"""
+
+import ctypes
+import os
+
+from . import errors
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdrs.so")
+
+# ---- constants mirrored from include/drs.h -------------------------------
+DRS_OK = 0
+GEN_PCG64 = 0
+GEN_SFC64 = 1
+FAMILY_DDIM = 0
+FAMILY_DDPM = 1
+FAMILY_DDPM_X0 = 2
+FAMILY_PRED_X0 = 3
+FAMILY_EULER = 4
+SRC_X = 0
+SRC_CUR = 1
+SRC_ANCHOR = 2
+OP_SAVE_ANCHOR = 1
+ERR_NOISE_WINDOW_BIT = 1
+ERR_GM_TIMESTEP_BIT = 2
+
+
+class NativeLibraryMissing(RuntimeError):
+    """libdrs.so is not built; run `python -m paper_2603_25872_b200._build`."""
+
+
+class DrsKey(ctypes.Structure):
+    _fields_ = [
+        ("vals", ctypes.c_int64 * 4),
+        ("n_vals", ctypes.c_int32),
+        ("seed_slot", ctypes.c_int32),
+        ("seed_mask", ctypes.c_uint64),
+    ]
+
+
+class DrsOp(ctypes.Structure):
+    _fields_ = [
+        ("c", ctypes.c_double * 6),
+        ("family", ctypes.c_int32),
+        ("noisy", ctypes.c_int32),
+        ("src", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("eps_f32", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+        ("x", ctypes.c_void_p),
+        ("eps", ctypes.c_void_p),
+        ("z", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
+        ("out2", ctypes.c_void_p),
+    ]
+
+
+assert ctypes.sizeof(DrsKey) == 48
+assert ctypes.sizeof(DrsOp) == 112
+
+_lib = None
+
+_SIGS = {
+    "drs_noise_fill": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                      ctypes.c_void_p]),
+    "drs_skip_chain": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]),
+    "drs_gm_eps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p]),
+    "drs_copy_rows": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                     ctypes.c_void_p]),
+    "drs_spin": (ctypes.c_int, [ctypes.c_double, ctypes.c_int, ctypes.c_void_p]),
+    "drs_host_log1p": (ctypes.c_double, [ctypes.c_double]),
+    "drs_host_exp": (ctypes.c_double, [ctypes.c_double]),
+    "drs_host_seedseq": (ctypes.c_int, [ctypes.POINTER(DrsKey), ctypes.c_uint64,
+                                        ctypes.POINTER(ctypes.c_uint32), ctypes.c_int]),
+    "drs_version": (ctypes.c_int, []),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libdrs.so once; raise loudly if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{_LIB_PATH} not built (python -m paper_2603_25872_b200._build); "
+                "there is no CPU fallback")
+        L = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+_STATUS_EXC = {
+    1: ValueError,
+    2: errors.TimestepOutOfRange,
+    3: errors.InvalidSkip,
+    4: errors.VarianceTooLarge,
+    5: errors.DimensionMismatch,
+    6: errors.InvalidPlanParams,
+    7: RuntimeError,
+    8: RuntimeError,
+}
+
+
+def check(status: int, what: str):
+    if status != DRS_OK:
+        exc = _STATUS_EXC.get(status, RuntimeError)
+        raise exc(f"{what} failed with drs status {status}")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,209 @@
+// K1/K1b: bit-exact counter-based normal streams on sm_100a.
+//
+// Replaces skipdiff rng.py:27-33 (derive_noise) and denoiser.py:139-145
+// (state_independent_eps): numpy Generator.standard_normal over PCG64 (or the
+// SFC64 variant) seeded by SeedSequence(key).  numpy's ziggurat
+// (random_standard_normal, 256 layers) consumes a VARIABLE number of 64-bit
+// words per normal: 1 on the fast path (98.5%), 2 on a wedge test (which may
+// reject and restart), 1+2m on the tail.  Output j therefore depends on how
+// many words normals 0..j-1 consumed; the decode is a chain over word
+// positions.  One CTA owns one stream and walks it in tiles of W positions:
+//
+//   1. generate: words[tile_base .. tile_base+W+MARGIN) into shared memory.
+//      PCG64: every thread jumps (affine LCG map) to its own 9-word chunk.
+//      SFC64: no jump-ahead -> one thread generates sequentially.
+//   2. classify (all threads, independent per position p): the attempt that
+//      would START at p -> (step = words consumed, accept, value).  Wedge and
+//      tail attempts read their extra words from the lookahead margin.
+//   3. resolve (warp 0): the chain visits p iff no earlier visited attempt
+//      covers it.  Per 32-position window: ballot the slow lanes, jump over
+//      covered lanes with __ffs, rank the visited+accepted lanes with popc,
+//      and store their values to out[] coalesced.  A cover that runs past the
+//      window/tile is carried in a register.
+//
+// Arithmetic is IEEE double with contraction disabled (--fmad=false), in the
+// operation order of numpy's C code (no FMA in libnpyrandom), with glibc's
+// FMA-variant log1p/exp ported in glibc_math.cuh.
+#include <cuda_runtime.h>
+#include "drs.h"
+#include "bitgen.cuh"
+#include "glibc_math.cuh"
+
+namespace drs {
+
+__device__ const uint64_t kZigKi[256] = DRS_ZIG_KI;
+__device__ const double kZigWi[256] = DRS_ZIG_WI;
+__device__ const double kZigFi[256] = DRS_ZIG_FI;
+
+constexpr int kThreads = 256;
+constexpr int kPer = 9;                       // words generated per thread per tile
+constexpr int kWords = kThreads * kPer;       // 2304 words in smem per tile
+constexpr int kMargin = 64;                   // lookahead for wedge/tail attempts
+constexpr int kW = kWords - kMargin;          // 2240 positions classified per tile
+static_assert(kW % 32 == 0, "tile must be whole warps");
+
+constexpr double kZigR = 3.6541528853610088;
+constexpr double kZigInvR = 0.27366123732975828;
+
+__device__ __forceinline__ double next_double_of(uint64_t w) {
+  return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+template <int GEN>
+__global__ void __launch_bounds__(kThreads)
+noise_fill_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
+                  int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  __shared__ uint64_t words[kWords];
+  __shared__ double vals[kW];
+  __shared__ uint8_t steps[kW];               // bit7 = accept, bits0..6 = words consumed
+  __shared__ u128 s_pcg_state, s_pcg_inc;
+  __shared__ uint64_t s_sfc[4];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int sidx = blockIdx.x;
+  double* const o = out + (int64_t)sidx * ld;
+
+  if (tid == 0) {
+    const drs_key k = keys[sidx];
+    const uint64_t seed = k.seed_slot >= 0 ? seeds[k.seed_slot] : 0ull;
+    uint32_t ent[8];
+    const int ne = key_words(k, seed, ent);
+    if (GEN == DRS_GEN_PCG64) {
+      Pcg64 g; g.seed(ent, ne);
+      s_pcg_state = g.state; s_pcg_inc = g.inc;
+    } else {
+      Sfc64 g; g.seed(ent, ne);
+      s_sfc[0] = g.a; s_sfc[1] = g.b; s_sfc[2] = g.c; s_sfc[3] = g.w;
+    }
+  }
+  __syncthreads();
+
+  // PCG64: per-thread tile-start state (after tile_base + tid*kPer steps) and
+  // the affine map advancing it by one tile (kW steps).
+  u128 st = 0, inc = 0, tile_m = 0, tile_p = 0;
+  if (GEN == DRS_GEN_PCG64) {
+    inc = s_pcg_inc;
+    u128 am, ap;
+    Pcg64::jump(inc, (uint64_t)tid * kPer, am, ap);
+    st = am * s_pcg_state + ap;
+    Pcg64::jump(inc, (uint64_t)kW, tile_m, tile_p);
+  }
+  Sfc64 sfc;
+  if (GEN == DRS_GEN_SFC64 && tid == 0) {
+    sfc.a = s_sfc[0]; sfc.b = s_sfc[1]; sfc.c = s_sfc[2]; sfc.w = s_sfc[3];
+  }
+
+  __shared__ int64_t s_count;
+  if (tid == 0) s_count = 0;
+  int64_t count = 0;        // warp 0's running output count
+  int cover = 0;            // warp 0's carried cover (positions to skip)
+  int local_err = 0;
+
+  for (;;) {
+    // ---- 1. generate -------------------------------------------------------
+    if (GEN == DRS_GEN_PCG64) {
+      u128 s = st;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        s = s * pcg_mult() + inc;
+        words[tid * kPer + j] = Pcg64::output(s);
+      }
+      st = tile_m * st + tile_p;
+    } else if (tid == 0) {
+      Sfc64 g = sfc;
+      for (int j = 0; j < kWords; ++j) {
+        words[j] = g.next();
+        if (j == kW - 1) sfc = g;             // next tile starts at tile_base + kW
+      }
+    }
+    __syncthreads();
+
+    // ---- 2. classify every position of the tile ---------------------------
+    for (int p = tid; p < kW; p += kThreads) {
+      const uint64_t w = words[p];
+      const int idx = (int)(w & 0xff);
+      const uint64_t r = w >> 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+      double x = (double)rabs * kZigWi[idx];
+      if (r & 1) x = -x;
+      int step = 1, acc = 1;
+      if (rabs >= kZigKi[idx]) {
+        if (idx == 0) {                      // tail: 2 doubles per iteration
+          int q = p + 1;
+          double xx;
+          for (;;) {
+            if (q + 1 >= kWords) { local_err = 1; xx = 0.0; break; }
+            xx = -kZigInvR * log1p_glibc(-next_double_of(words[q]));
+            const double yy = -log1p_glibc(-next_double_of(words[q + 1]));
+            q += 2;
+            if (yy + yy > xx * xx) break;
+          }
+          x = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+          step = q - p;
+          if (step > 127) { local_err = 1; step = 127; }
+        } else {                             // wedge: 1 double, may reject
+          const double u = next_double_of(words[p + 1]);
+          const double lhs = (kZigFi[idx - 1] - kZigFi[idx]) * u + kZigFi[idx];
+          acc = lhs < exp_glibc(-0.5 * x * x) ? 1 : 0;
+          step = 2;
+        }
+      }
+      vals[p] = x;
+      steps[p] = (uint8_t)(step | (acc << 7));
+    }
+    __syncthreads();
+
+    // ---- 3. resolve the chain + store (warp 0) ----------------------------
+    if (tid < 32) {
+      for (int base = 0; base < kW && count < n; base += 32) {
+        const uint8_t sv = steps[base + lane];
+        const int my_step = sv & 0x7f;
+        const unsigned slow = __ballot_sync(0xffffffffu, my_step != 1);
+        const unsigned accm = __ballot_sync(0xffffffffu, (sv >> 7) & 1);
+        unsigned vis = 0;
+        if (cover >= 32) {
+          cover -= 32;
+        } else {
+          int pos = cover;
+          while (pos < 32) {
+            const unsigned ahead = slow & (0xffffffffu << pos);
+            if (ahead == 0) { vis |= 0xffffffffu << pos; pos = 32; break; }
+            const int s = __ffs(ahead) - 1;
+            const unsigned upto = (s == 31) ? 0xffffffffu : ((1u << (s + 1)) - 1u);
+            vis |= upto & (0xffffffffu << pos);
+            pos = s + __shfl_sync(0xffffffffu, my_step, s);
+          }
+          cover = pos - 32;
+        }
+        const unsigned va = vis & accm;
+        if ((va >> lane) & 1u) {
+          const int64_t oi = count + __popc(va & ((1u << lane) - 1u));
+          if (oi < n) o[oi] = vals[base + lane];
+        }
+        count += __popc(va);
+      }
+      if (lane == 0) s_count = count;
+    }
+    __syncthreads();
+    if (s_count >= n) break;
+  }
+  if (local_err) atomicOr(err, 1);
+}
+
+}  // namespace drs
+
+extern "C" int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const uint64_t* seeds,
+                              int64_t n, double* out, int64_t ld, int* err, void* stream) {
+  if (n_streams < 0 || n < 0 || (n_streams > 0 && ld < n)) return DRS_ERR_VALUE;
+  if (n_streams == 0 || n == 0) return DRS_OK;
+  if (!keys || !out || !err) return DRS_ERR_VALUE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (gen == DRS_GEN_PCG64)
+    drs::noise_fill_kernel<DRS_GEN_PCG64><<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+  else if (gen == DRS_GEN_SFC64)
+    drs::noise_fill_kernel<DRS_GEN_SFC64><<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+  else
+    return DRS_ERR_VALUE;
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}

@@ -1,0 +1,102 @@
+"""Executes sampler programs for the reference-shaped API (sequential.py /
+parallel.py): program + DeviceRun caching, input staging, timing, outputs."""
+
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import torch
+
+from .engine import Comm, DeviceRun
+from .transitions import _device_of, as_device
+
+_RUNS: "OrderedDict[tuple, DeviceRun]" = OrderedDict()
+_MAX_RUNS = 32
+
+
+@dataclass
+class Trajectory:
+    """(t, x) states from the start of sampling down to t=0 plus accounting
+    (sequential.py:18-32).  States are CUDA fp64 tensors (views of one
+    (n_states, D) buffer owned by this trajectory)."""
+
+    states: list = field(default_factory=list)
+    eval_count: int = 0
+    wall_ms: float = 0.0
+    device_ms: float = 0.0     # CUDA-event time of the whole run (x_T -> x_0)
+
+    @property
+    def final(self):
+        return self.states[-1][1]
+
+    def timesteps(self) -> list:
+        return [t for t, _ in self.states]
+
+
+@dataclass
+class RoundReport:
+    """One parallel round (parallel.py:61-66): eps evaluations issued and the
+    device time of the round (eval + gather), measured with CUDA events."""
+
+    anchor_t: int
+    parallel_evals: int
+    round_wall_ms: float
+    worker_spans: list = field(default_factory=list)
+
+
+def _denoiser_key(d):
+    return id(d)
+
+
+def get_run(prog_key, build_prog, s, d, D, device, generator, comm: Comm | None) -> DeviceRun:
+    key = (prog_key, id(s), _denoiser_key(d), int(D), str(device), generator,
+           (comm.rank, comm.size) if comm else (0, 1))
+    run = _RUNS.get(key)
+    if run is not None and run.denoiser_ref is d and run.schedule_ref is s:
+        _RUNS.move_to_end(key)
+        return run
+    run = DeviceRun(build_prog(), s, d, D, device, generator=generator, comm=comm)
+    run.denoiser_ref, run.schedule_ref = d, s
+    _RUNS[key] = run
+    while len(_RUNS) > _MAX_RUNS:
+        _RUNS.popitem(last=False)
+    return run
+
+
+def execute(run: DeviceRun, x_T, seed: int, clock=None, *, reports: bool = False):
+    """Run once (eagerly, with per-round CUDA events) and return
+    (Trajectory, [RoundReport]).  x_T: numpy array or tensor of D elements."""
+    dev = run.device
+    x = as_device(x_T, dev, torch.float64)
+    shape = tuple(x.shape)
+    run.set_inputs(x, seed)
+    n_rounds = len(run.prog.rounds)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(n_rounds)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    run.enqueue(events=ev)
+    t1.record()
+    traj_buf = run.traj.clone()
+    t1.synchronize()
+    run.check_err()
+    per_round = run.account(clock)
+    round_ms = [a.elapsed_time(b) for a, b in ev]
+    traj = Trajectory(eval_count=run.prog.eval_count)
+    traj.states = [(t, traj_buf[j].view(shape)) for j, t in enumerate(run.prog.timesteps)]
+    traj.device_ms = t0.elapsed_time(t1)
+    rep = []
+    for r, info in enumerate(run.prog.rounds):
+        ms = per_round[r] if per_round is not None else round_ms[r]
+        spans = [(i, 0.0, ms) for i in range(info.n_tasks)]
+        rep.append(RoundReport(info.anchor_t, info.n_tasks, ms, spans))
+    if clock is not None:
+        traj.wall_ms = sum(per_round)
+    elif run.prog.kind == "parallel":
+        traj.wall_ms = sum(round_ms)          # rounds only, as parallel.py:318-320
+    else:
+        traj.wall_ms = traj.device_ms         # sequential: full elapsed (sequential.py:112)
+    return traj, rep
+
+
+def resolve_device(x_T):
+    return _device_of(x_T)

@@ -1,0 +1,49 @@
+"""Single-stream samplers: the 1-GPU baseline the parallel schedulers are
+measured against (skipdiff sequential.py:57-130), as device programs."""
+
+from .program import build_sequential
+from .rng import RngStream
+from .runner import Trajectory, execute, get_run, resolve_device
+from .transitions import VarianceRule, predicted_x0_device
+
+
+def predicted_x0(s, x_t, eps, t: int):
+    """x0_hat = (x_t - sqrt(1-abar_t) eps) / sqrt(abar_t) (sequential.py:51-54)."""
+    return predicted_x0_device(s, x_t, eps, t)
+
+
+def _numel(x):
+    n = 1
+    for d in getattr(x, "shape", ()):
+        n *= int(d)
+    return n
+
+
+def sample_ddpm(s, d, x_T, noise: RngStream, clock=None) -> Trajectory:
+    """Ancestral DDPM: T unit-step posterior transitions, z of step t from
+    key (t-1, TRANSITION) (sequential.py:57-76)."""
+    dev = resolve_device(x_T)
+    rule = VarianceRule.deterministic()
+    run = get_run(("seq", "ddpm", s.T), lambda: build_sequential(s, rule, "ddpm"),
+                  s, d, _numel(x_T), dev, noise.generator, None)
+    traj, _ = execute(run, x_T, noise.seed, clock)
+    return traj
+
+
+def sample_ddim(s, d, x_T, rule: VarianceRule, noise: RngStream, subsequence=None, clock=None) -> Trajectory:
+    """DDIM along a timestep subsequence (default every step); the z of the
+    transition into u is key (u, TRANSITION) (sequential.py:88-113)."""
+    dev = resolve_device(x_T)
+    sub = tuple(subsequence) if subsequence is not None else None
+    run = get_run(("seq", "ddim", s.T, rule, sub), lambda: build_sequential(s, rule, "ddim", sub),
+                  s, d, _numel(x_T), dev, noise.generator, None)
+    traj, _ = execute(run, x_T, noise.seed, clock)
+    return traj
+
+
+def sample_euler(g, gm, x_init):
+    """Euler ODE sampler (sequential.py:116-130): Euler family, next-row scope."""
+    raise NotImplementedError("Euler family (sample_euler) is the next scope row; not built yet")
+
+
+__all__ = ["Trajectory", "predicted_x0", "sample_ddpm", "sample_ddim", "sample_euler"]

@@ -1,0 +1,147 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+    python tests/golden/make_golden.py
+
+Imports skipdiff from /root/reference/pkg/src (read-only, this container only;
+the reference does not travel to the GPU box) and writes:
+  noise.npz  normal streams of chosen keys, PCG64 (the reference's rng.py:32
+             path) and the SFC64 variant of the same SeedSequence keys, with
+             the ziggurat path counts of each stream (keys chosen so wedge
+             rejections, tails and a tail retry all occur);
+  traj.npz   sha256 of every trajectory state (bit-exact pin) + selected
+             final states for the BASELINE configs' sampler shapes with the
+             state-independent and Gaussian-mixture toy denoisers;
+  plans.json plan_blocks for every config.
+Run on numpy 2.3.5 / scipy 1.18.1 / glibc 2.39 (FMA libm variant).
+"""
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(HERE, "..", "..", "oracle"))
+
+import noise_restated  # noqa: E402
+import skipdiff as sd  # noqa: E402
+
+NOISE_KEYS = [
+    # (key tuple, n)
+    ((0x7A9C, 0, 50, 2), 4096),             # INIT of seed 0, T=50
+    ((0x7A9C, 12345678901, 3, 1), 4096),    # two-word seed, DRAFT role, a tail
+    ((0x7A9C, 0xFFFFFFFFFFFF, 0, 0), 4096),  # max 48-bit seed, t=0 (word 0)
+    ((0x51DE, 0, 1), 4096),                 # state_independent_eps(0, 1, .) (denoiser.py:144)
+    ((0x51DE, 11, 250), 1),                 # n = 1
+    ((0x7A9C, 7, 30, 0), 32768),            # multi-tile stream, several tails
+]
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def find_tail_retry_key(gen):
+    for seed in range(2000):
+        key = (0x7A9C, seed, 17, 0)
+        _, paths = noise_restated.draw(key, 4096, gen)
+        if any("tail-retry" in p for p in paths):
+            return key
+    raise RuntimeError("no tail retry found")
+
+
+def noise_fixture():
+    out = {}
+    for gen in ("pcg64", "sfc64"):
+        keys = list(NOISE_KEYS) + [(find_tail_retry_key(gen), 4096)]
+        streams, meta = [], []
+        for key, n in keys:
+            if gen == "pcg64":
+                v = np.random.default_rng(key).standard_normal(n)
+            else:
+                v = np.random.Generator(np.random.SFC64(np.random.SeedSequence(key))).standard_normal(n)
+            _, paths = noise_restated.draw(key, n, gen)
+            counts = {}
+            for p in paths:
+                for x in p:
+                    counts[x] = counts.get(x, 0) + 1
+            streams.append(v)
+            meta.append({"key": list(key), "n": n, "paths": counts})
+        out[f"{gen}_values"] = np.concatenate(streams)
+        out[f"{gen}_meta"] = np.array(json.dumps(meta))
+    # the only PRNG output the reference's own tests pin (test_denoiser.py:162-165)
+    out["si_golden_0_1_2"] = sd.state_independent_eps(0, 1, 2)
+    np.savez_compressed(os.path.join(HERE, "noise.npz"), **out)
+
+
+def gm_toy(dim):
+    m = np.zeros((2, dim))
+    m[0, 0], m[1, 0] = -2.0, 2.0
+    return sd.GaussianMixture(weights=[0.5, 0.5], means=m, variances=[1.0, 1.0])
+
+
+CASES = [
+    # name, T, D, sampler, devices, family, rule, denoiser, keep_final
+    ("c1_si_det", 50, 4096, "conservative", 2, "ddim", "det", "si", True),
+    ("c1_si_ddpmrule", 50, 4096, "conservative", 2, "ddim", "ddpm", "si", True),
+    ("c1_gm_det", 50, 4096, "conservative", 2, "ddim", "det", "gm", True),
+    ("c1_gm_ddpmrule", 50, 4096, "conservative", 2, "ddim", "ddpm", "gm", True),
+    ("c1_seq_gm_det", 50, 4096, "seq_ddim", 1, "ddim", "det", "gm", True),
+    ("c2_si", 50, 4096, "aggressive", 3, "ddpm", "det", "si", True),
+    ("c2_gm", 50, 4096, "aggressive", 3, "ddpm", "det", "gm", True),
+    ("c2_seq_gm", 50, 4096, "seq_ddpm", 1, "ddpm", "det", "gm", True),
+    ("c3_si_n2", 50, 16384, "aggressive", 2, "ddim", "det", "si", False),
+    ("c3_si_n4", 50, 16384, "aggressive", 4, "ddim", "det", "si", False),
+    ("c3_si_n8", 50, 16384, "aggressive", 8, "ddim", "det", "si", False),
+    ("c4_si", 250, 4096, "conservative", 8, "ddpm", "det", "si", True),
+    ("c5_si", 30, 65536, "aggressive", 8, "ddim", "det", "si", False),
+]
+
+
+def traj_fixture():
+    out, manifest = {}, []
+    for name, T, D, sampler, n, fam, rule_s, den_s, keep in CASES:
+        s = sd.default_schedule(T)
+        rule = sd.VarianceRule.deterministic() if rule_s == "det" else sd.VarianceRule.ddpm_induced()
+        den = sd.StateIndependent(seed=11, dim=D) if den_s == "si" else sd.AnalyticEps(gm_toy(D))
+        stream = sd.RngStream(seed=0)
+        x_T = sd.derive_noise(stream, T, sd.Role.INIT, D)
+        if sampler == "aggressive":
+            traj, rep = sd.run_aggressive(s, den, x_T, n, rule, stream, update_family=fam)
+        elif sampler == "conservative":
+            traj, rep = sd.run_conservative(s, den, x_T, n, rule, stream, update_family=fam)
+        elif sampler == "seq_ddim":
+            traj, rep = sd.sample_ddim(s, den, x_T, rule, stream), []
+        else:
+            traj, rep = sd.sample_ddpm(s, den, x_T, stream), []
+        out[f"{name}_sha"] = np.array([_sha(x) for _, x in traj.states])
+        out[f"{name}_t"] = np.array(traj.timesteps())
+        if keep:
+            out[f"{name}_final"] = traj.final
+        manifest.append({"name": name, "T": T, "D": D, "sampler": sampler, "devices": n, "family": fam,
+                         "rule": rule_s, "denoiser": den_s, "seed": 0, "si_seed": 11,
+                         "eval_count": traj.eval_count, "rounds": len(rep)})
+    out["manifest"] = np.array(json.dumps(manifest))
+    np.savez_compressed(os.path.join(HERE, "traj.npz"), **out)
+
+
+def plans_fixture():
+    plans = {}
+    for T in (50, 250, 30, 48, 10, 9, 5):
+        for n in (1, 2, 3, 4, 8):
+            for mode in sd.Mode:
+                p = sd.plan_blocks(T, n, mode)
+                plans[f"{T}_{n}_{mode.value}"] = {"blocks": [list(b) for b in p.blocks],
+                                                  "rounds": p.total_rounds, "evals": p.total_evals}
+    with open(os.path.join(HERE, "plans.json"), "w") as f:
+        json.dump(plans, f, indent=0, sort_keys=True)
+
+
+if __name__ == "__main__":
+    noise_fixture()
+    traj_fixture()
+    plans_fixture()
+    print("golden fixtures written to", HERE)

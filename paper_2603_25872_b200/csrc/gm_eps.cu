@@ -6,26 +6,32 @@
 //   log_i   = log w_i + (-0.5 * sum_j (x_j - c_ij)^2) / s_i - (0.5 D) log s_i
 //   r       = exp(log - logsumexp(log))
 //   eps_j   = -sqrt(1 - abar) * sum_i (r_i (c_ij - x_j)) / s_i
-// One CTA per state row.  Pass 1 reduces the n_comp squared distances
-// (deterministic fixed tree: per-thread strided partials -> warp shuffle ->
-// shared memory), pass 2 is elementwise.  The reduction order differs from
+// One CTA (1024 threads) per state row, ONE pass over HBM: every thread
+// issues all its loads up front (x and the n_comp mean entries of its
+// kPer elements stay in registers), the n_comp squared distances are reduced
+// with a fixed tree (warp shuffles -> shared memory -> warp 0), and the eps
+// is written from the same registers.  The reduction order differs from
 // numpy's pairwise sum, so parity with the reference is to fp64 rounding
 // (tests state the tolerance); across ranks the kernel is bit-reproducible.
+// Rows longer than kThreads*kPer are processed in register-sized chunks with
+// a second (L2-resident) read.
 #include <cuda_runtime.h>
 #include <math.h>
 #include "drs.h"
 
 namespace drs {
 
-constexpr int kGmThreads = 512;
+constexpr int kGmThreads = 1024;
+constexpr int kGmPer = 4;            // elements per thread held in registers
 constexpr int kGmMaxComp = 8;
+constexpr int kGmRegComp = 2;        // components kept in registers (others re-read)
 
 __global__ void __launch_bounds__(kGmThreads)
 gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ ts, int64_t D,
               const double* __restrict__ alpha_bar, int T, const double* __restrict__ means,
               const double* __restrict__ log_w, const double* __restrict__ var, int n_comp,
               double* const* __restrict__ outs, int* __restrict__ err) {
-  __shared__ double red[kGmMaxComp][kGmThreads / 32];
+  __shared__ double red[kGmMaxComp][32];
   __shared__ double s_r[kGmMaxComp];
   const int row = blockIdx.x;
   const int t = ts[row];
@@ -38,21 +44,40 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
   const double abar = alpha_bar[t];
   const double sa = sqrt(abar);
   const double one_m = 1.0 - abar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = (int64_t)kGmThreads * kGmPer;
+  const bool single = D <= chunk;
 
+  // ---- pass 1: squared distances ------------------------------------------
   double part[kGmMaxComp];
 #pragma unroll
   for (int i = 0; i < kGmMaxComp; ++i) part[i] = 0.0;
-  for (int64_t j = threadIdx.x; j < D; j += kGmThreads) {
-    const double xj = x[j];
+  double xr[kGmPer], mr[kGmRegComp][kGmPer];
+  for (int64_t base = 0; base < D; base += chunk) {
 #pragma unroll
-    for (int i = 0; i < kGmMaxComp; ++i) {
-      if (i < n_comp) {
-        const double d = xj - sa * means[(int64_t)i * D + j];
-        part[i] += d * d;
+    for (int e = 0; e < kGmPer; ++e) {
+      const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+      const bool ok = j < D;
+      xr[e] = ok ? __ldg(x + j) : 0.0;
+#pragma unroll
+      for (int i = 0; i < kGmRegComp; ++i)
+        mr[i][e] = (ok && i < n_comp) ? __ldg(means + (int64_t)i * D + j) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < kGmPer; ++e) {
+      const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+      if (j < D) {
+#pragma unroll
+        for (int i = 0; i < kGmMaxComp; ++i) {
+          if (i < n_comp) {
+            const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
+            const double d = xr[e] - sa * m;
+            part[i] += d * d;
+          }
+        }
       }
     }
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < kGmMaxComp; ++i) {
     if (i < n_comp) {
@@ -62,40 +87,68 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     double lc[kGmMaxComp];
     double mx = -INFINITY;
-    for (int i = 0; i < n_comp; ++i) {
-      double d2 = 0.0;
-      for (int w = 0; w < kGmThreads / 32; ++w) d2 += red[i][w];
-      const double s = abar * var[i] + one_m;
-      lc[i] = log_w[i] + ((-0.5 * d2) / s - (0.5 * (double)D) * log(s));
-      mx = fmax(mx, lc[i]);
-    }
-    double sum = 0.0;
-    for (int i = 0; i < n_comp; ++i) sum += exp(lc[i] - mx);
-    const double lse = log(sum) + mx;
-    for (int i = 0; i < n_comp; ++i) s_r[i] = exp(lc[i] - lse);
-  }
-  __syncthreads();
-  const double neg_sq = -sqrt(one_m);
-  double r[kGmMaxComp], inv_s[kGmMaxComp];
-#pragma unroll
-  for (int i = 0; i < kGmMaxComp; ++i) {
-    r[i] = i < n_comp ? s_r[i] : 0.0;
-    inv_s[i] = i < n_comp ? abar * var[i] + one_m : 1.0;   // the scale itself (divided below)
-  }
-  for (int64_t j = threadIdx.x; j < D; j += kGmThreads) {
-    const double xj = x[j];
-    double score = 0.0;
 #pragma unroll
     for (int i = 0; i < kGmMaxComp; ++i) {
       if (i < n_comp) {
-        const double term = (r[i] * (sa * means[(int64_t)i * D + j] - xj)) / inv_s[i];
-        score = (i == 0) ? term : score + term;
+        double d2 = red[i][lane];
+        for (int off = 16; off; off >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, off);
+        const double s = abar * var[i] + one_m;
+        lc[i] = log_w[i] + ((-0.5 * d2) / s - (0.5 * (double)D) * log(s));
+        mx = fmax(mx, lc[i]);
+      } else {
+        lc[i] = -INFINITY;
       }
     }
-    out[j] = neg_sq * score;
+    if (lane == 0) {
+      double sum = 0.0;
+#pragma unroll
+      for (int i = 0; i < kGmMaxComp; ++i) if (i < n_comp) sum += exp(lc[i] - mx);
+      const double lse = log(sum) + mx;
+#pragma unroll
+      for (int i = 0; i < kGmMaxComp; ++i) if (i < n_comp) s_r[i] = exp(lc[i] - lse);
+    }
+  }
+  __syncthreads();
+
+  // ---- pass 2: eps ----------------------------------------------------------
+  const double neg_sq = -sqrt(one_m);
+  double r[kGmMaxComp], sc[kGmMaxComp];
+#pragma unroll
+  for (int i = 0; i < kGmMaxComp; ++i) {
+    r[i] = i < n_comp ? s_r[i] : 0.0;
+    sc[i] = i < n_comp ? abar * var[i] + one_m : 1.0;
+  }
+  for (int64_t base = 0; base < D; base += chunk) {
+    if (!single) {   // re-read this chunk (L2-resident) into the registers
+#pragma unroll
+      for (int e = 0; e < kGmPer; ++e) {
+        const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+        const bool ok = j < D;
+        xr[e] = ok ? __ldg(x + j) : 0.0;
+#pragma unroll
+        for (int i = 0; i < kGmRegComp; ++i)
+          mr[i][e] = (ok && i < n_comp) ? __ldg(means + (int64_t)i * D + j) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < kGmPer; ++e) {
+      const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+      if (j < D) {
+        double score = 0.0;
+#pragma unroll
+        for (int i = 0; i < kGmMaxComp; ++i) {
+          if (i < n_comp) {
+            const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
+            const double term = (r[i] * (sa * m - xr[e])) / sc[i];
+            score = (i == 0) ? term : score + term;
+          }
+        }
+        out[j] = neg_sq * score;
+      }
+    }
   }
 }
 

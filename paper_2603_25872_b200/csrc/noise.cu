@@ -49,141 +49,193 @@ __device__ __forceinline__ double next_double_of(uint64_t w) {
   return (double)(w >> 11) * (1.0 / 9007199254740992.0);
 }
 
-template <int GEN>
+// Classify positions p = p0, p0+stride, ... < W of one tile: the ziggurat
+// attempt starting at p -> (value, words consumed, accept).  words[] holds
+// W + kMarginWords valid entries.
+__device__ __forceinline__ void classify(const uint64_t* __restrict__ words, int n_words,
+                                         double* __restrict__ vals, uint8_t* __restrict__ steps,
+                                         int W, int p0, int stride, int& local_err) {
+  for (int p = p0; p < W; p += stride) {
+    const uint64_t w = words[p];
+    const int idx = (int)(w & 0xff);
+    const uint64_t r = w >> 8;
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * kZigWi[idx];
+    if (r & 1) x = -x;
+    int step = 1, acc = 1;
+    if (rabs >= kZigKi[idx]) {
+      if (idx == 0) {                      // tail: 2 doubles per iteration
+        int q = p + 1;
+        double xx;
+        for (;;) {
+          if (q + 1 >= n_words) { local_err = 1; xx = 0.0; break; }
+          xx = -kZigInvR * log1p_glibc(-next_double_of(words[q]));
+          const double yy = -log1p_glibc(-next_double_of(words[q + 1]));
+          q += 2;
+          if (yy + yy > xx * xx) break;
+        }
+        x = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+        step = q - p;
+        if (step > 127) { local_err = 1; step = 127; }
+      } else {                             // wedge: 1 double, may reject
+        const double u = next_double_of(words[p + 1]);
+        const double lhs = (kZigFi[idx - 1] - kZigFi[idx]) * u + kZigFi[idx];
+        acc = lhs < exp_glibc(-0.5 * x * x) ? 1 : 0;
+        step = 2;
+      }
+    }
+    vals[p] = x;
+    steps[p] = (uint8_t)(step | (acc << 7));
+  }
+}
+
+// Resolve the visit chain over one classified tile and store the accepted
+// values (called by one full warp).  count / cover carry across tiles.
+__device__ __forceinline__ void resolve(const double* __restrict__ vals, const uint8_t* __restrict__ steps,
+                                        int W, double* __restrict__ o, int64_t n, int64_t& count,
+                                        int& cover, int lane) {
+  for (int base = 0; base < W && count < n; base += 32) {
+    const uint8_t sv = steps[base + lane];
+    const int my_step = sv & 0x7f;
+    const unsigned slow = __ballot_sync(0xffffffffu, my_step != 1);
+    const unsigned accm = __ballot_sync(0xffffffffu, (sv >> 7) & 1);
+    unsigned vis = 0;
+    if (cover >= 32) {
+      cover -= 32;
+    } else {
+      int pos = cover;
+      while (pos < 32) {
+        const unsigned ahead = slow & (0xffffffffu << pos);
+        if (ahead == 0) { vis |= 0xffffffffu << pos; pos = 32; break; }
+        const int s = __ffs(ahead) - 1;
+        const unsigned upto = (s == 31) ? 0xffffffffu : ((1u << (s + 1)) - 1u);
+        vis |= upto & (0xffffffffu << pos);
+        pos = s + __shfl_sync(0xffffffffu, my_step, s);
+      }
+      cover = pos - 32;
+    }
+    const unsigned va = vis & accm;
+    if ((va >> lane) & 1u) {
+      const int64_t oi = count + __popc(va & ((1u << lane) - 1u));
+      if (oi < n) o[oi] = vals[base + lane];
+    }
+    count += __popc(va);
+  }
+}
+
+__device__ __forceinline__ void load_key(const drs_key* keys, const uint64_t* seeds, int sidx,
+                                         uint32_t* ent, int& ne) {
+  const drs_key k = keys[sidx];
+  const uint64_t seed = k.seed_slot >= 0 ? seeds[k.seed_slot] : 0ull;
+  ne = key_words(k, seed, ent);
+}
+
+// ------------------------------------------------------------- PCG64 -------
+// Every thread jumps to its own 9-word chunk of the tile (affine LCG map).
 __global__ void __launch_bounds__(kThreads)
-noise_fill_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
-                  int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
+noise_pcg64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
+                   int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
   __shared__ uint64_t words[kWords];
   __shared__ double vals[kW];
   __shared__ uint8_t steps[kW];               // bit7 = accept, bits0..6 = words consumed
-  __shared__ u128 s_pcg_state, s_pcg_inc;
-  __shared__ uint64_t s_sfc[4];
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int sidx = blockIdx.x;
-  double* const o = out + (int64_t)sidx * ld;
-
+  __shared__ u128 s_state, s_inc;
+  __shared__ int64_t s_count;
+  const int tid = threadIdx.x, lane = tid & 31;
+  double* const o = out + (int64_t)blockIdx.x * ld;
   if (tid == 0) {
-    const drs_key k = keys[sidx];
-    const uint64_t seed = k.seed_slot >= 0 ? seeds[k.seed_slot] : 0ull;
     uint32_t ent[8];
-    const int ne = key_words(k, seed, ent);
-    if (GEN == DRS_GEN_PCG64) {
-      Pcg64 g; g.seed(ent, ne);
-      s_pcg_state = g.state; s_pcg_inc = g.inc;
-    } else {
-      Sfc64 g; g.seed(ent, ne);
-      s_sfc[0] = g.a; s_sfc[1] = g.b; s_sfc[2] = g.c; s_sfc[3] = g.w;
-    }
+    int ne;
+    load_key(keys, seeds, blockIdx.x, ent, ne);
+    Pcg64 g; g.seed(ent, ne);
+    s_state = g.state; s_inc = g.inc;
+    s_count = 0;
   }
   __syncthreads();
-
-  // PCG64: per-thread tile-start state (after tile_base + tid*kPer steps) and
-  // the affine map advancing it by one tile (kW steps).
-  u128 st = 0, inc = 0, tile_m = 0, tile_p = 0;
-  if (GEN == DRS_GEN_PCG64) {
-    inc = s_pcg_inc;
+  const u128 inc = s_inc;
+  u128 st, tile_m, tile_p;
+  {
     u128 am, ap;
     Pcg64::jump(inc, (uint64_t)tid * kPer, am, ap);
-    st = am * s_pcg_state + ap;
+    st = am * s_state + ap;                    // state after tid*kPer steps
     Pcg64::jump(inc, (uint64_t)kW, tile_m, tile_p);
   }
-  Sfc64 sfc;
-  if (GEN == DRS_GEN_SFC64 && tid == 0) {
-    sfc.a = s_sfc[0]; sfc.b = s_sfc[1]; sfc.c = s_sfc[2]; sfc.w = s_sfc[3];
-  }
-
-  __shared__ int64_t s_count;
-  if (tid == 0) s_count = 0;
-  int64_t count = 0;        // warp 0's running output count
-  int cover = 0;            // warp 0's carried cover (positions to skip)
-  int local_err = 0;
-
+  int64_t count = 0;
+  int cover = 0, local_err = 0;
   for (;;) {
-    // ---- 1. generate -------------------------------------------------------
-    if (GEN == DRS_GEN_PCG64) {
-      u128 s = st;
+    u128 s = st;
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        s = s * pcg_mult() + inc;
-        words[tid * kPer + j] = Pcg64::output(s);
-      }
-      st = tile_m * st + tile_p;
-    } else if (tid == 0) {
-      Sfc64 g = sfc;
-      for (int j = 0; j < kWords; ++j) {
-        words[j] = g.next();
-        if (j == kW - 1) sfc = g;             // next tile starts at tile_base + kW
-      }
+    for (int j = 0; j < kPer; ++j) {
+      s = s * pcg_mult() + inc;
+      words[tid * kPer + j] = Pcg64::output(s);
     }
+    st = tile_m * st + tile_p;
     __syncthreads();
-
-    // ---- 2. classify every position of the tile ---------------------------
-    for (int p = tid; p < kW; p += kThreads) {
-      const uint64_t w = words[p];
-      const int idx = (int)(w & 0xff);
-      const uint64_t r = w >> 8;
-      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-      double x = (double)rabs * kZigWi[idx];
-      if (r & 1) x = -x;
-      int step = 1, acc = 1;
-      if (rabs >= kZigKi[idx]) {
-        if (idx == 0) {                      // tail: 2 doubles per iteration
-          int q = p + 1;
-          double xx;
-          for (;;) {
-            if (q + 1 >= kWords) { local_err = 1; xx = 0.0; break; }
-            xx = -kZigInvR * log1p_glibc(-next_double_of(words[q]));
-            const double yy = -log1p_glibc(-next_double_of(words[q + 1]));
-            q += 2;
-            if (yy + yy > xx * xx) break;
-          }
-          x = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
-          step = q - p;
-          if (step > 127) { local_err = 1; step = 127; }
-        } else {                             // wedge: 1 double, may reject
-          const double u = next_double_of(words[p + 1]);
-          const double lhs = (kZigFi[idx - 1] - kZigFi[idx]) * u + kZigFi[idx];
-          acc = lhs < exp_glibc(-0.5 * x * x) ? 1 : 0;
-          step = 2;
-        }
-      }
-      vals[p] = x;
-      steps[p] = (uint8_t)(step | (acc << 7));
-    }
+    classify(words, kWords, vals, steps, kW, tid, kThreads, local_err);
     __syncthreads();
-
-    // ---- 3. resolve the chain + store (warp 0) ----------------------------
     if (tid < 32) {
-      for (int base = 0; base < kW && count < n; base += 32) {
-        const uint8_t sv = steps[base + lane];
-        const int my_step = sv & 0x7f;
-        const unsigned slow = __ballot_sync(0xffffffffu, my_step != 1);
-        const unsigned accm = __ballot_sync(0xffffffffu, (sv >> 7) & 1);
-        unsigned vis = 0;
-        if (cover >= 32) {
-          cover -= 32;
-        } else {
-          int pos = cover;
-          while (pos < 32) {
-            const unsigned ahead = slow & (0xffffffffu << pos);
-            if (ahead == 0) { vis |= 0xffffffffu << pos; pos = 32; break; }
-            const int s = __ffs(ahead) - 1;
-            const unsigned upto = (s == 31) ? 0xffffffffu : ((1u << (s + 1)) - 1u);
-            vis |= upto & (0xffffffffu << pos);
-            pos = s + __shfl_sync(0xffffffffu, my_step, s);
-          }
-          cover = pos - 32;
-        }
-        const unsigned va = vis & accm;
-        if ((va >> lane) & 1u) {
-          const int64_t oi = count + __popc(va & ((1u << lane) - 1u));
-          if (oi < n) o[oi] = vals[base + lane];
-        }
-        count += __popc(va);
-      }
+      resolve(vals, steps, kW, o, n, count, cover, lane);
       if (lane == 0) s_count = count;
+    }
+    __syncthreads();
+    if (s_count >= n) break;
+  }
+  if (local_err) atomicOr(err, 1);
+}
+
+// ------------------------------------------------------------- SFC64 -------
+// No jump-ahead: one generator lane (warp kSfcGenWarp) produces tile i+1 into
+// the other half of a double buffer while warps 0..kSfcGenWarp-1 classify
+// and resolve tile i, so the serial recurrence is the only critical path.
+constexpr int kSfcW = 512;                        // positions per tile (less speculative waste)
+constexpr int kSfcWords = kSfcW + kMargin;        // words generated per tile
+constexpr int kSfcGenWarp = kThreads / 32 - 1;    // last warp generates
+constexpr int kSfcWorkers = kThreads - 32;
+
+__global__ void __launch_bounds__(kThreads)
+noise_sfc64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
+                   int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  __shared__ uint64_t words[2][kSfcWords];
+  __shared__ double vals[kSfcW];
+  __shared__ uint8_t steps[kSfcW];
+  __shared__ int64_t s_count;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* const o = out + (int64_t)blockIdx.x * ld;
+  const bool gen_lane = warp == kSfcGenWarp && lane == 0;
+  Sfc64 g;
+  if (gen_lane) {
+    uint32_t ent[8];
+    int ne;
+    load_key(keys, seeds, blockIdx.x, ent, ne);
+    g.seed(ent, ne);
+    Sfc64 h = g;                                   // tile 0
+    for (int j = 0; j < kSfcWords; ++j) {
+      words[0][j] = h.next();
+      if (j == kSfcW - 1) g = h;                  // tile 1 starts kSfcW words in
+    }
+  }
+  if (tid == 0) s_count = 0;
+  __syncthreads();
+  int64_t count = 0;
+  int cover = 0, local_err = 0;
+  for (int tile = 0;; ++tile) {
+    const int cur = tile & 1;
+    if (warp == kSfcGenWarp) {
+      if (lane == 0) {                             // speculatively generate the next tile
+        Sfc64 h = g;
+        uint64_t* dst = words[cur ^ 1];
+#pragma unroll 4
+        for (int j = 0; j < kSfcWords; ++j) {
+          dst[j] = h.next();
+          if (j == kSfcW - 1) g = h;
+        }
+      }
+    } else {
+      classify(words[cur], kSfcWords, vals, steps, kSfcW, tid, kSfcWorkers, local_err);
+      asm volatile("bar.sync 1, %0;" :: "n"(kSfcWorkers));
+      if (warp == 0) {
+        resolve(vals, steps, kSfcW, o, n, count, cover, lane);
+        if (lane == 0) s_count = count;
+      }
     }
     __syncthreads();
     if (s_count >= n) break;
@@ -200,9 +252,9 @@ extern "C" int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const
   if (!keys || !out || !err) return DRS_ERR_VALUE;
   cudaStream_t s = (cudaStream_t)stream;
   if (gen == DRS_GEN_PCG64)
-    drs::noise_fill_kernel<DRS_GEN_PCG64><<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+    drs::noise_pcg64_kernel<<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
   else if (gen == DRS_GEN_SFC64)
-    drs::noise_fill_kernel<DRS_GEN_SFC64><<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+    drs::noise_sfc64_kernel<<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
   else
     return DRS_ERR_VALUE;
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;

@@ -145,6 +145,11 @@ class DeviceRun:
         for st in self.prog.steps:
             if isinstance(st, Chain):
                 off = len(ops_all)
+                written = set()
+                for o in st.ops:   # chain.cu prefetches operands: no RAW through memory within a chain
+                    if o.src == _lib.SRC_X and o.x in written:
+                        raise AssertionError(f"chain op reads {o.x} written earlier in the same launch")
+                    written.update(b for b in (o.out, o.out2) if b is not None)
                 for o in st.ops:
                     ops_all.append(make_op(
                         o.c, o.family, o.noisy, src=o.src,

@@ -56,9 +56,12 @@ def _run_case(m, cuda, generator="pcg64"):
 
 def test_golden_trajectories(cuda, golden_dir):
     """SI denoiser: every state bit-identical to the reference run (sha256 of
-    each state).  GM denoiser: the eps reduction order differs from numpy's
-    pairwise sum, so states are compared to the oracle per step within
-    rel-L2 <= 1e-12 and max-abs <= 1e-11 (fp64)."""
+    each state).  GM denoiser: the squared-distance reduction order differs
+    from numpy's pairwise sum (and numpy's SIMD log/exp are host-dependent),
+    so d2 ~ 4e3 carries ~1e-13 absolute rounding that the softmax turns into
+    ~1e-13 relative eps error, amplified up to 1/sqrt(abar_T) ~ 360 along the
+    trajectory: states are compared to the oracle per step within
+    rel-L2 <= 1e-10 and max-abs <= 1e-9 (fp64)."""
     z = np.load(os.path.join(golden_dir, "traj.npz"))
     for m in json.loads(str(z["manifest"])):
         traj, rep = _run_case(m, cuda)
@@ -84,7 +87,7 @@ def test_golden_trajectories(cuda, golden_dir):
             for (_, g), (_, r) in zip(traj.states, ref):
                 g = _np(g)
                 rel = np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-300)
-                assert rel <= 1e-12 and np.max(np.abs(g - r)) <= 1e-11, (m["name"], rel)
+                assert rel <= 1e-10 and np.max(np.abs(g - r)) <= 1e-9, (m["name"], rel)
 
 
 @pytest.mark.parametrize("family", ["ddim", "ddpm"])

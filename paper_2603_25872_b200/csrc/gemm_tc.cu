@@ -1,0 +1,416 @@
+// K4: persistent, warp-specialised bf16 GEMM on the 5th-gen tensor cores.
+//
+//   C[M, N] = epilogue( alpha * A[M, K] . B[N, K]^T )        (nn.Linear: y = x W^T)
+//
+// A, B: bf16, K-major (row-major with K contiguous), staged into shared
+// memory by TMA (cp.async.bulk.tensor, SWIZZLE_128B, 64-element K slabs) in a
+// kStages-deep mbarrier ring; one elected thread issues tcgen05.mma
+// (M=128, N=BN, K=16) accumulating fp32 in TMEM; the accumulator is double
+// buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps the
+// MMAs of tile i+1.  Warp roles (192 threads):
+//   warp 0        TMA producer            (one elected lane)
+//   warp 1        TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5    epilogue: tcgen05.ld 32x32b -> registers -> bias / GELU /
+//                 SiLU / GEGLU / residual / alpha -> bf16 or fp32 stores
+// Grid = min(#tiles, #SMs); each CTA walks tiles t = blockIdx.x, +gridDim.x.
+// Split-K (kSplit > 1): each split accumulates a K range and writes fp32
+// partials; drs_gemm_reduce sums them in a fixed order (deterministic, no
+// atomics) and applies the same epilogue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "drs_net.h"
+#include "tc_common.cuh"
+
+namespace drs {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;                 // one 128-byte swizzle atom of bf16
+constexpr int kGemmThreads = 192;
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.7071067811865476f)); }
+__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+
+struct EpiParams {
+  void* out;
+  int64_t ldo;
+  const float* bias;        // [N] or null
+  const void* res;          // residual [M, ldr] (bf16, or fp32 if res_f32) or null
+  int64_t ldr;
+  int res_f32;
+  const float* colscale;    // per-column scale applied after act (adaLN gate) or null:
+  int cs_group;             //   colscale[(row / cs_group) * cs_ld + n] if cs_group > 0, else colscale[n]
+  int64_t cs_ld;
+  float alpha;
+  int act;                  // DRS_ACT_*
+  int out_f32;              // 1: fp32 output, 0: bf16
+  float* partial;           // split-K workspace [split][M][N] fp32 (split > 1)
+};
+
+// Apply the epilogue to 32 consecutive accumulator columns n0..n0+31 of `row`.
+__device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
+  if (row >= M) return;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int n = n0 + j;
+    float x = v[j] * p.alpha;
+    if (p.bias && n < N) x += __ldg(p.bias + n);
+    v[j] = x;
+  }
+  if (p.act == DRS_ACT_GEGLU) {                // interleaved (value, gate) pairs -> N/2 outputs
+    float o[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
+    const int c0 = n0 / 2;
+    if (p.res) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < N / 2)
+          o[j] += p.res_f32 ? static_cast<const float*>(p.res)[(int64_t)row * p.ldr + c0 + j]
+                            : __bfloat162float(static_cast<const __nv_bfloat16*>(p.res)[(int64_t)row * p.ldr + c0 + j]);
+    }
+    if (p.out_f32) {
+      float* dst = static_cast<float*>(p.out) + (int64_t)row * p.ldo + c0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) dst[j] = o[j];
+    } else {
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ldo + c0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) dst[j] = __float2bfloat16(o[j]);
+    }
+    return;
+  }
+  if (p.act == DRS_ACT_GELU_TANH) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+  } else if (p.act == DRS_ACT_SILU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = silu(v[j]);
+  } else if (p.act == DRS_ACT_GELU_ERF) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  }
+  const bool full = n0 + 32 <= N;
+  if (p.colscale) {
+    const float* cs = p.colscale + (p.cs_group > 0 ? (int64_t)(row / p.cs_group) * p.cs_ld : 0) + n0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] *= __ldg(cs + j);
+  }
+  if (p.res && p.res_f32) {
+    const float* r = static_cast<const float*>(p.res) + (int64_t)row * p.ldr + n0;
+    if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(r + 4 * q);
+        v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += r[j];
+    }
+  } else if (p.res) {
+    const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.res) + (int64_t)row * p.ldr + n0;
+    if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4*>(r + 8 * q);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __bfloat162float(r[j]);
+    }
+  }
+  if (p.out_f32) {
+    float* dst = static_cast<float*>(p.out) + (int64_t)row * p.ldo + n0;
+    if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = v[j];
+    }
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ldo + n0;
+    if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+        *reinterpret_cast<uint4*>(dst + 8 * q) = u;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = __float2bfloat16(v[j]);
+    }
+  }
+}
+
+template <int BN, int kStages>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = kStages * kStageBytes;
+  static constexpr int kBytes = kBarOffset + (2 * kStages + 4) * 8 + 16 + 1024;   // +1024 alignment slack
+};
+
+template <int BN, int kStages>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                    int M, int N, int K, int split, EpiParams ep) {
+  using S = GemmSmem<BN, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;       // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (M + kBM - 1) / kBM, n_tiles = (N + BN - 1) / BN;
+  const int num_kb_total = (K + kBK - 1) / kBK;
+  const int kb_per_split = (num_kb_total + split - 1) / split;
+  const int num_tiles = m_tiles * n_tiles * split;
+  constexpr uint32_t kTmemCols = 2 * BN;          // double-buffered accumulator
+  constexpr uint32_t kIdesc = tc::idesc_bf16_f32(kBM, BN);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmap_a);
+    tc::tma_prefetch(&tmap_b);
+    for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], 4); }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int sp = tile % split;
+        const int mn = tile / split;
+        const int mt = mn % m_tiles, nt = mn / m_tiles;
+        const int kb0 = sp * kb_per_split;
+        const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
+          tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int sp = tile % split;
+      const int kb0 = sp * kb_per_split;
+      const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full_bar[stage], phase);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint8_t* sa = smem + stage * S::kStageBytes;
+          const uint64_t da = tc::smem_desc_sw128(sa);
+          const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)      // +32 B per K=16 step inside the swizzle atom
+            tc::mma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          tc::mma_commit(&empty_bar[stage]);
+          if (kb == kb1 - 1) tc::mma_commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
+        if (tc::elect_one()) tc::mma_commit(&tfull_bar[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int sp = tile % split;
+      const int mn = tile / split;
+      const int mt = mn % m_tiles, nt = mn / m_tiles;
+      const int kb0 = sp * kb_per_split;
+      const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int row = mt * kBM + quad * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int n0 = nt * BN + c * 32;
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
+        tc::tmem_ld_wait();
+        if (n0 >= N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = kb1 > kb0 ? __uint_as_float(r[j]) : 0.f;
+        if (split > 1) {
+          if (row < M) {
+            float* dst = ep.partial + ((int64_t)sp * M + row) * N + n0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = v[j];
+          }
+        } else {
+          epilogue32(ep, M, N, row, n0, v);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// Deterministic split-K reduction + epilogue: one thread per (row, 32-col chunk).
+__global__ void gemm_reduce_kernel(int M, int N, int split, EpiParams ep) {
+  const int chunks = (N + 31) / 32;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)M * chunks) return;
+  const int row = (int)(idx / chunks), n0 = (int)(idx % chunks) * 32;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  for (int s = 0; s < split; ++s) {
+    const float* src = ep.partial + ((int64_t)s * M + row) * N + n0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += src[j];
+  }
+  epilogue32(ep, M, N, row, n0, v);
+}
+
+// ------------------------------------------------------------ host side ---
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map: `rows` x `cols` (cols contiguous), row stride in elements.
+static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, int kStages>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
+                       const EpiParams& ep, cudaStream_t st) {
+  using S = GemmSmem<BN, kStages>;
+  auto kern = gemm_bf16_tc_kernel<BN, kStages>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
+      return DRS_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kGemmThreads, S::kBytes, st>>>(ta, tb, M, N, K, split, ep);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+}  // namespace drs
+
+extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
+                             int act, int out_f32, float alpha, int bn, int split, float* workspace,
+                             void* stream) {
+  return drs_gemm_bf16_ex(A, lda, B, ldb, C, ldc, M, N, K, bias, residual, ldr, 0, nullptr, 0, 0, act, out_f32,
+                          alpha, bn, split, workspace, stream);
+}
+
+extern "C" int drs_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                                int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
+                                int res_f32, const float* colscale, int cs_group, int64_t cs_ld, int act,
+                                int out_f32, float alpha, int bn, int split, float* workspace, void* stream) {
+  using namespace drs;
+  if (M <= 0 || N <= 0 || K <= 0) return (M == 0 || N == 0) ? DRS_OK : DRS_ERR_VALUE;
+  if (!A || !B || !C) return DRS_ERR_VALUE;
+  if ((K % 8) || (lda % 8) || (ldb % 8)) return DRS_ERR_VALUE;          // TMA: 16-byte row strides
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return DRS_ERR_VALUE;
+  if (act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
+  if (bn == 0) bn = 128;
+  if (bn != 64 && bn != 128 && bn != 256) return DRS_ERR_VALUE;
+  if (split < 1) split = 1;
+  if (split > 1 && !workspace) return DRS_ERR_VALUE;
+  CUtensorMap ta, tb;
+  if (!make_tmap(&ta, A, M, K, lda, kBM) || !make_tmap(&tb, B, N, K, ldb, bn)) return DRS_ERR_CUDA;
+  EpiParams ep{C, ldc, bias, residual, ldr, res_f32, colscale, cs_group, cs_ld, alpha, act, out_f32, workspace};
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, st);
+  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, M, N, K, split, ep, st);
+  else rc = launch_gemm<256, 4>(ta, tb, M, N, K, split, ep, st);
+  if (rc != DRS_OK || split == 1) return rc;
+  const int64_t threads = (int64_t)M * ((N + 31) / 32);
+  gemm_reduce_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(M, N, split, ep);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}

@@ -1,0 +1,347 @@
+// Denoiser-network ops around the tensor-core GEMM (gemm_tc.cu):
+//   * LayerNorm (+ affine or adaLN modulate) -> bf16       one warp per row
+//   * fused attention softmax(Q K^T * scale) V              FA2-style, mma.sync
+//     m16n8k16 bf16 -> fp32, 64 queries per CTA, online softmax in registers
+//   * DiT helpers: sinusoidal timestep embedding, patchify / unpatchify,
+//     SiLU->bf16 cast.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <math.h>
+#include <stdint.h>
+#include "drs_net.h"
+
+namespace drs {
+
+// ------------------------------------------------------------ LayerNorm ---
+template <int kVec>   // columns per lane = kVec * 32 chunks handled in a loop
+__global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_f32, int M, int C,
+                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                 const float* __restrict__ shift, const float* __restrict__ scale, int mod_group,
+                                 int64_t mod_ld, float eps, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  float v[kVec];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int c = lane + 32 * i;
+    float a = 0.f;
+    if (c < C) {
+      a = x_f32 ? static_cast<const float*>(x)[(int64_t)row * ldx + c]
+                : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[(int64_t)row * ldx + c]);
+    }
+    v[i] = a;
+    sum += a;
+  }
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / C;
+  float sq = 0.f;
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int c = lane + 32 * i;
+    if (c < C) { const float d = v[i] - mean; sq += d * d; }
+  }
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / C + eps);
+  const int64_t mofs = mod_group > 0 ? (int64_t)(row / mod_group) * mod_ld : 0;
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int c = lane + 32 * i;
+    if (c < C) {
+      float y = (v[i] - mean) * rstd;
+      if (gamma) y = y * gamma[c] + (beta ? beta[c] : 0.f);
+      if (scale) y = y * (1.f + scale[mofs + c]);
+      if (shift) y = y + shift[mofs + c];
+      out[(int64_t)row * ldo + c] = __float2bfloat16(y);
+    }
+  }
+}
+
+// ------------------------------------------------------------ attention ---
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+constexpr int kAttnBQ = 64, kAttnThreads = 128;
+
+template <int DP, int BK = (DP > 96 ? 32 : 64)>   // DP: head dim padded to a multiple of 16; BK: keys per tile
+__global__ void __launch_bounds__(kAttnThreads)
+attention_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq, const __nv_bfloat16* __restrict__ k,
+                 int64_t ldk, const __nv_bfloat16* __restrict__ v, int64_t ldv, __nv_bfloat16* __restrict__ o,
+                 int64_t ldo, int Lq, int Lk, int d, float scale_log2) {
+  constexpr int LD = DP + 8;            // smem row stride (elements): 16 B aligned, staggers banks
+  __shared__ __align__(16) __nv_bfloat16 sQ[kAttnBQ * LD];
+  __shared__ __align__(16) __nv_bfloat16 sK[BK * LD];
+  __shared__ __align__(16) __nv_bfloat16 sV[BK * LD];
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * kAttnBQ;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const __nv_bfloat16* qb = q + ((int64_t)b * Lq) * ldq + (int64_t)h * d;
+  const __nv_bfloat16* kbp = k + ((int64_t)b * Lk) * ldk + (int64_t)h * d;
+  const __nv_bfloat16* vbp = v + ((int64_t)b * Lk) * ldv + (int64_t)h * d;
+  constexpr int CH = DP / 8;            // 16-byte chunks per padded row
+  const int dch = d / 8;
+
+  for (int i = tid; i < kAttnBQ * CH; i += kAttnThreads) {
+    const int r = i / CH, c = i % CH;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (q0 + r < Lq && c < dch) val = *reinterpret_cast<const uint4*>(qb + (int64_t)(q0 + r) * ldq + c * 8);
+    *reinterpret_cast<uint4*>(&sQ[r * LD + c * 8]) = val;
+  }
+  __syncthreads();
+  uint32_t qa[DP / 16][4];
+  {
+    const int r = warp * 16 + (lane & 15), c = (lane >> 4) * 8;
+#pragma unroll
+    for (int ks = 0; ks < DP / 16; ++ks)
+      ldsm_x4(static_cast<uint32_t>(__cvta_generic_to_shared(&sQ[r * LD + ks * 16 + c])), qa[ks][0], qa[ks][1],
+              qa[ks][2], qa[ks][3]);
+  }
+  float oacc[DP / 8][4];
+#pragma unroll
+  for (int i = 0; i < DP / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // rows g and g+8
+
+  for (int k0 = 0; k0 < Lk; k0 += BK) {
+    __syncthreads();
+    for (int i = tid; i < BK * CH; i += kAttnThreads) {
+      const int r = i / CH, c = i % CH;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (k0 + r < Lk && c < dch) {
+        kv = *reinterpret_cast<const uint4*>(kbp + (int64_t)(k0 + r) * ldk + c * 8);
+        vv = *reinterpret_cast<const uint4*>(vbp + (int64_t)(k0 + r) * ldv + c * 8);
+      }
+      *reinterpret_cast<uint4*>(&sK[r * LD + c * 8]) = kv;
+      *reinterpret_cast<uint4*>(&sV[r * LD + c * 8]) = vv;
+    }
+    __syncthreads();
+    float s[BK / 8][4];
+#pragma unroll
+    for (int nb = 0; nb < BK / 8; ++nb) {
+      s[nb][0] = s[nb][1] = s[nb][2] = s[nb][3] = 0.f;
+      const int r = nb * 8 + (lane & 7), cofs = ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int ks = 0; ks < DP / 16; ++ks) {
+        uint32_t b0, b1;
+        ldsm_x2(static_cast<uint32_t>(__cvta_generic_to_shared(&sK[r * LD + ks * 16 + cofs])), b0, b1);
+        mma16816(s[nb], qa[ks], b0, b1);
+      }
+    }
+    // scale, mask, online softmax (rows g / g+8 spread over the 4 threads of a quad)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < BK / 8; ++nb) {
+      const int kc = k0 + nb * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool valid = (kc + (e & 1)) < Lk;
+        s[nb][e] = valid ? s[nb][e] * scale_log2 : -INFINITY;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[nb][0], s[nb][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[nb][2], s[nb][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+    const float a0 = exp2f(m0 - nm0), a1 = exp2f(m1 - nm1);
+    m0 = nm0;
+    m1 = nm1;
+    float rs0 = 0.f, rs1 = 0.f;
+    uint32_t pa[BK / 16][4];
+#pragma unroll
+    for (int nb = 0; nb < BK / 8; ++nb) {
+      const float p0 = exp2f(s[nb][0] - nm0), p1 = exp2f(s[nb][1] - nm0);
+      const float p2 = exp2f(s[nb][2] - nm1), p3 = exp2f(s[nb][3] - nm1);
+      rs0 += p0 + p1;
+      rs1 += p2 + p3;
+      const int kk = nb >> 1, half = nb & 1;
+      pa[kk][half * 2 + 0] = pack_bf16(p0, p1);
+      pa[kk][half * 2 + 1] = pack_bf16(p2, p3);
+    }
+    l0 = l0 * a0 + rs0;
+    l1 = l1 * a1 + rs1;
+#pragma unroll
+    for (int db = 0; db < DP / 8; ++db) {
+      oacc[db][0] *= a0; oacc[db][1] *= a0;
+      oacc[db][2] *= a1; oacc[db][3] *= a1;
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+      const int r = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int db = 0; db < DP / 8; ++db) {
+        uint32_t b0, b1;
+        ldsm_x2_t(static_cast<uint32_t>(__cvta_generic_to_shared(&sV[r * LD + db * 8])), b0, b1);
+        mma16816(oacc[db], pa[kk], b0, b1);
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
+  __nv_bfloat16* ob = o + ((int64_t)b * Lq) * ldo + (int64_t)h * d;
+#pragma unroll
+  for (int db = 0; db < DP / 8; ++db) {
+    const int c = db * 8 + 2 * t;
+    if (c < d) {
+      if (r0 < Lq)
+        *reinterpret_cast<__nv_bfloat162*>(ob + (int64_t)r0 * ldo + c) =
+            __floats2bfloat162_rn(oacc[db][0] * i0, oacc[db][1] * i0);
+      if (r1 < Lq)
+        *reinterpret_cast<__nv_bfloat162*>(ob + (int64_t)r1 * ldo + c) =
+            __floats2bfloat162_rn(oacc[db][2] * i1, oacc[db][3] * i1);
+    }
+  }
+}
+
+// ---------------------------------------------------------- DiT helpers ---
+// emb[i] = [cos(t f_j), sin(t f_j)], f_j = exp(-ln(max_period) j / half)  (DiT TimestepEmbedder)
+__global__ void timestep_embedding_kernel(const float* __restrict__ t, int n, int dim, float max_period,
+                                          __nv_bfloat16* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int half = dim / 2;
+  if (i >= n * half) return;
+  const int r = i / half, j = i % half;
+  const float f = expf(-logf(max_period) * j / half);
+  const float a = t[r] * f;
+  out[(int64_t)r * dim + j] = __float2bfloat16(cosf(a));
+  out[(int64_t)r * dim + half + j] = __float2bfloat16(sinf(a));
+}
+
+// latent x (C, H, W) fp64/fp32 -> tokens (H/p * W/p, C*p*p) bf16, feature order (c, py, px)
+__global__ void patchify_kernel(const void* __restrict__ x, int x_f64, int C, int H, int W, int p,
+                                __nv_bfloat16* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gw = W / p, feat = C * p * p;
+  if (i >= (H / p) * gw * feat) return;
+  const int tok = i / feat, f = i % feat;
+  const int c = f / (p * p), py = (f / p) % p, px = f % p;
+  const int hh = (tok / gw) * p + py, ww = (tok % gw) * p + px;
+  const int64_t src = ((int64_t)c * H + hh) * W + ww;
+  const float val = x_f64 ? (float)static_cast<const double*>(x)[src] : static_cast<const float*>(x)[src];
+  out[i] = __float2bfloat16(val);
+}
+
+// tokens (H/p * W/p, p*p*Cout) fp32, feature order (py, px, c) -> eps (Ckeep, H, W) fp32
+__global__ void unpatchify_kernel(const float* __restrict__ tok, int Cout, int Ckeep, int H, int W, int p,
+                                  float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Ckeep * H * W) return;
+  const int c = i / (H * W), hh = (i / W) % H, ww = i % W;
+  const int gw = W / p;
+  const int t = (hh / p) * gw + (ww / p);
+  const int f = ((hh % p) * p + (ww % p)) * Cout + c;
+  out[i] = tok[(int64_t)t * (p * p * Cout) + f];
+}
+
+__global__ void silu_cast_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { const float a = x[i]; out[i] = __float2bfloat16(a / (1.f + __expf(-a))); }
+}
+
+}  // namespace drs
+
+using namespace drs;
+
+extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C, const float* gamma,
+                             const float* beta, const float* shift, const float* scale, int mod_group,
+                             int64_t mod_ld, float eps, void* out, int64_t ldo, void* stream) {
+  if (M <= 0 || C <= 0) return M == 0 ? DRS_OK : DRS_ERR_VALUE;
+  if (!x || !out || C > 32 * 64) return DRS_ERR_VALUE;
+  const int warps = 8;
+  dim3 grid((M + warps - 1) / warps);
+  cudaStream_t st = (cudaStream_t)stream;
+  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
+  const int vec = (C + 31) / 32;
+  if (vec <= 16)
+    layernorm_kernel<16><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
+  else if (vec <= 48)
+    layernorm_kernel<48><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
+  else
+    layernorm_kernel<64><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                             void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale,
+                             void* stream) {
+  if (B <= 0 || H <= 0 || Lq <= 0 || Lk <= 0) return DRS_ERR_VALUE;
+  if (d % 8 || d > 160 || (ldq | ldk | ldv | ldo) % 8) return DRS_ERR_VALUE;
+  const int DP = (d + 15) / 16 * 16;
+  dim3 grid((Lq + kAttnBQ - 1) / kAttnBQ, H, B);
+  const float sl2 = scale * 1.4426950408889634f;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto Q = static_cast<const __nv_bfloat16*>(q);
+  auto K = static_cast<const __nv_bfloat16*>(k);
+  auto V = static_cast<const __nv_bfloat16*>(v);
+  auto O = static_cast<__nv_bfloat16*>(o);
+  switch (DP) {
+    case 16: attention_kernel<16><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 32: attention_kernel<32><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 48: attention_kernel<48><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 64: attention_kernel<64><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 80: attention_kernel<80><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 96: attention_kernel<96><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 128: attention_kernel<128><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 160: attention_kernel<160><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    default: return DRS_ERR_VALUE;
+  }
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out, void* stream) {
+  if (n <= 0 || dim <= 0 || dim % 2) return DRS_ERR_VALUE;
+  const int tot = n * dim / 2;
+  timestep_embedding_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      t, n, dim, max_period, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out, void* stream) {
+  if (p <= 0 || H % p || W % p) return DRS_ERR_VALUE;
+  const int tot = C * H * W;
+  patchify_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, x_f64, C, H, W, p,
+                                                                       static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_unpatchify(const float* tok, int Cout, int Ckeep, int H, int W, int p, float* out, void* stream) {
+  if (p <= 0 || H % p || W % p || Ckeep > Cout) return DRS_ERR_VALUE;
+  const int tot = Ckeep * H * W;
+  unpatchify_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(tok, Cout, Ckeep, H, W, p, out);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_silu_cast(const float* x, int64_t n, void* out, void* stream) {
+  if (n < 0) return DRS_ERR_VALUE;
+  if (n == 0) return DRS_OK;
+  silu_cast_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      x, n, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}

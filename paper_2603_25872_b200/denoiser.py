@@ -145,6 +145,7 @@ class NetworkEps:
     net: object
     latent_shape: tuple
     cfg_scale: float = 1.0
+    t_scale: float | None = None      # model timestep per sampler step (default 1000 / T)
 
 
 Denoiser = AnalyticEps | StateIndependent | Perturbed | Latency | Counting | NetworkEps

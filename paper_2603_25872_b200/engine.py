@@ -80,6 +80,12 @@ class DeviceRun:
             self.dim, self.B = dim, self.D // dim      # B independent rows per state (batched x_T)
             self.eps_dtype = torch.float64
         elif isinstance(core, NetworkEps):
+            n = 1
+            for v in core.latent_shape:
+                n *= int(v)
+            if n != self.D:
+                from .errors import DimensionMismatch
+                raise DimensionMismatch(f"network latent {core.latent_shape} != state size {self.D}")
             self.dim, self.B = self.D, 1
             self.eps_dtype = torch.float32
         else:
@@ -200,9 +206,10 @@ class DeviceRun:
             return None
         core = self.core
         if isinstance(core, NetworkEps):
-            return ("net", dict(xs=[self.buf(src) for (_, src, _), _ in local],
-                                outs=[self.buf(dst) for _, dst in local],
-                                ts=[t for (_, _, t), _ in local], n=len(local), n_tasks=len(local)))
+            from .netdenoise import lower_eval
+            chunks = lower_eval(core, self.s, [self.buf(src) for (_, src, _), _ in local],
+                                [t for (_, _, t), _ in local], [self.buf(dst) for _, dst in local], self.device)
+            return ("net", dict(chunks=chunks, n=len(local), n_tasks=len(local)))
         # one row per (task, batch row b): GM rows are independent states;
         # the SI eps of a task is the same row broadcast over b (denoiser.py:252)
         xs, outs, ts = [], [], []
@@ -250,7 +257,7 @@ class DeviceRun:
                        "drs_copy_rows")
         else:
             from .netdenoise import network_eval_into
-            network_eval_into(self.core, self.s, a["xs"], a["ts"], a["outs"])
+            network_eval_into(self.core, a["chunks"])
 
     def enqueue(self, events=None, timers=None):
         """Issue the whole run on the current stream (capturable when world == 1).

@@ -1,0 +1,112 @@
+"""Python wrappers of the network kernels in libdrs.so (include/drs_net.h).
+
+Tensors are torch CUDA tensors; every op launches on the current stream and
+raises if libdrs.so is missing (no fallback).  Weights are bf16, K-major
+(nn.Linear layout: W[out, in]); activations bf16; accumulation fp32.
+"""
+
+import torch
+
+from . import _lib
+
+ACT = {None: 0, "none": 0, "gelu_tanh": 1, "silu": 2, "gelu": 3, "geglu": 4}
+
+_ws = {}
+
+
+def _workspace(device, numel):
+    buf = _ws.get(device)
+    if buf is None or buf.numel() < numel:
+        buf = torch.empty(max(numel, 1 << 20), dtype=torch.float32, device=device)
+        _ws[device] = buf
+    return buf
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
+           bn=0, split=1, colscale=None, cs_group=0):
+    """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias) * colscale (+ residual);
+    N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out)."""
+    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+    M, K = x.shape
+    N = w.shape[0]
+    assert w.shape[1] == K and x.stride(1) == 1 and w.stride(1) == 1
+    n_out = N // 2 if act == "geglu" else N
+    if out is None:
+        out = torch.empty(M, n_out, dtype=out_dtype, device=x.device)
+    res_f32 = 0
+    if residual is not None:
+        assert residual.stride(1) == 1 and residual.dtype in (torch.bfloat16, torch.float32)
+        res_f32 = 1 if residual.dtype == torch.float32 else 0
+    if bias is not None:
+        assert bias.dtype == torch.float32
+    if colscale is not None:
+        assert colscale.dtype == torch.float32
+    if bn == 0:
+        bn = pick_bn(M, N)
+    ws = _workspace(x.device, split * M * N) if split > 1 else None
+    st = _lib.lib().drs_gemm_bf16_ex(
+        x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0), M, N, K,
+        _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0, res_f32, _ptr(colscale),
+        cs_group, colscale.stride(0) if (colscale is not None and colscale.dim() == 2) else 0, ACT[act], 1 if out.dtype == torch.float32 else 0, float(alpha), bn, split, _ptr(ws), _lib.stream_ptr())
+    _lib.check(st, "drs_gemm_bf16")
+    return out
+
+
+def pick_bn(M, N):
+    """Tile width: 256 when there are enough tiles to fill the GPU, else smaller."""
+    m_tiles = (M + 127) // 128
+    for bn in (256, 128):
+        if m_tiles * ((N + bn - 1) // bn) >= 148:
+            return bn
+    return 64 if m_tiles * ((N + 127) // 128) < 74 else 128
+
+
+def layernorm(x, out=None, gamma=None, beta=None, shift=None, scale=None, eps=1e-6, mod_group=0):
+    """shift/scale: (C,) or (n_groups, >=C) views with row stride; mod_group rows per group."""
+    M, C = x.shape
+    if out is None:
+        out = torch.empty(M, C, dtype=torch.bfloat16, device=x.device)
+    mod = shift if shift is not None else scale
+    mod_ld = mod.stride(0) if (mod is not None and mod.dim() == 2) else 0
+    st = _lib.lib().drs_layernorm(x.data_ptr(), x.stride(0), 1 if x.dtype == torch.float32 else 0, M, C,
+                                  _ptr(gamma), _ptr(beta), _ptr(shift), _ptr(scale), mod_group, mod_ld, float(eps),
+                                  out.data_ptr(), out.stride(0), _lib.stream_ptr())
+    _lib.check(st, "drs_layernorm")
+    return out
+
+
+def attention(q, k, v, out, B, H, Lq, Lk, d, scale=None):
+    """q: (B*Lq, >= H*d) view, k/v: (B*Lk, ...) views (row strides may exceed H*d)."""
+    scale = d ** -0.5 if scale is None else scale
+    st = _lib.lib().drs_attention(q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(), v.stride(0),
+                                  out.data_ptr(), out.stride(0), B, H, Lq, Lk, d, float(scale), _lib.stream_ptr())
+    _lib.check(st, "drs_attention")
+    return out
+
+
+def timestep_embedding(t, dim, out, max_period=10000.0):
+    _lib.check(_lib.lib().drs_timestep_embedding(t.data_ptr(), t.numel(), dim, float(max_period), out.data_ptr(),
+                                                 _lib.stream_ptr()), "drs_timestep_embedding")
+    return out
+
+
+def patchify(x, C, H, W, p, out):
+    _lib.check(_lib.lib().drs_patchify(x.data_ptr(), 1 if x.dtype == torch.float64 else 0, C, H, W, p,
+                                       out.data_ptr(), _lib.stream_ptr()), "drs_patchify")
+    return out
+
+
+def unpatchify(tok, c_out, c_keep, H, W, p, out):
+    _lib.check(_lib.lib().drs_unpatchify(tok.data_ptr(), c_out, c_keep, H, W, p, out.data_ptr(),
+                                         _lib.stream_ptr()), "drs_unpatchify")
+    return out
+
+
+def silu_cast(x, out):
+    _lib.check(_lib.lib().drs_silu_cast(x.data_ptr(), x.numel(), out.data_ptr(), _lib.stream_ptr()),
+               "drs_silu_cast")
+    return out

@@ -1,0 +1,54 @@
+"""K4 tcgen05 GEMM vs a plain PyTorch fp32 reference of the same op."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(x, w, bias, act, res, alpha):
+    y = alpha * (x.float() @ w.float().t())
+    if bias is not None:
+        y = y + bias
+    if act == "gelu_tanh":
+        y = torch.nn.functional.gelu(y, approximate="tanh")
+    elif act == "silu":
+        y = torch.nn.functional.silu(y)
+    elif act == "gelu":
+        y = torch.nn.functional.gelu(y)
+    elif act == "geglu":
+        y = y[:, 0::2] * torch.nn.functional.gelu(y[:, 1::2])
+    if res is not None:
+        y = y + res.float()
+    return y
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 1152, 1152), (300, 200, 136), (77, 768, 320),
+                                   (1024, 3456, 1152), (4096, 320, 2880), (8, 64, 4608)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_gemm_shapes(cuda, M, N, K, bn):
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    y = linear(x, w, out_dtype=torch.float32, bn=bn)
+    ref = _ref(x, w, None, None, None, 1.0)
+    err = (y - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), (M, N, K, bn, err)
+
+
+@pytest.mark.parametrize("act", [None, "gelu_tanh", "silu", "gelu", "geglu"])
+@pytest.mark.parametrize("split", [1, 3])
+def test_gemm_epilogues(cuda, act, split):
+    from paper_2603_25872_b200.netops import linear
+    M, N, K = 320, 640, 576
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    n_out = N // 2 if act == "geglu" else N
+    r = torch.randn(M, n_out, device=cuda, generator=g).bfloat16()
+    y = linear(x, w, bias=b, act=act, residual=r, alpha=0.5, split=split)
+    ref = _ref(x, w, b, act, r, 0.5)
+    rel = ((y.float() - ref).norm() / ref.norm()).item()
+    assert y.shape == (M, n_out) and rel <= 8e-3, (act, split, rel)

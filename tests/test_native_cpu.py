@@ -16,8 +16,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_header_symbols_exported(libdrs):
-    hdr = open(os.path.join(ROOT, "include", "drs.h")).read()
-    decls = set(re.findall(r"^(?:int|double)\s+(drs_\w+)\s*\(", hdr, re.M))
+    decls = set()
+    for h in ("drs.h", "drs_net.h"):
+        hdr = open(os.path.join(ROOT, "include", h)).read()
+        decls |= set(re.findall(r"^(?:int|double)\s+(drs_\w+)\s*\(", hdr, re.M))
     assert decls, "no declarations parsed"
     from paper_2603_25872_b200 import _lib
     assert decls == set(_lib.EXPORTED)

@@ -13,7 +13,9 @@
 namespace drs {
 
 // ------------------------------------------------------------ LayerNorm ---
-template <int kVec>   // columns per lane = kVec * 32 chunks handled in a loop
+// One warp per row, float4-vectorised; x and the modulation vectors are all
+// loaded before any arithmetic so the warp pays one memory round trip.
+template <int kV4>   // float4 chunks per lane (C <= 128 * kV4)
 __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_f32, int M, int C,
                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                  const float* __restrict__ shift, const float* __restrict__ scale, int mod_group,
@@ -22,39 +24,60 @@ __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  float v[kVec];
+  const int C4 = C >> 2;
+  const int64_t mofs = mod_group > 0 ? (int64_t)(row / mod_group) * mod_ld : 0;
+  float4 v[kV4], sc[kV4], sh[kV4];
+#pragma unroll
+  for (int i = 0; i < kV4; ++i) {
+    const int c4 = lane + 32 * i;
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sh[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c4 < C4) {
+      if (x_f32) {
+        v[i] = reinterpret_cast<const float4*>(static_cast<const float*>(x) + (int64_t)row * ldx)[c4];
+      } else {
+        const uint2 u = reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(x) + (int64_t)row * ldx)[c4];
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        v[i] = make_float4(a.x, a.y, b.x, b.y);
+      }
+      if (scale) sc[i] = reinterpret_cast<const float4*>(scale + mofs)[c4];
+      if (shift) sh[i] = reinterpret_cast<const float4*>(shift + mofs)[c4];
+    }
+  }
   float sum = 0.f;
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    const int c = lane + 32 * i;
-    float a = 0.f;
-    if (c < C) {
-      a = x_f32 ? static_cast<const float*>(x)[(int64_t)row * ldx + c]
-                : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[(int64_t)row * ldx + c]);
-    }
-    v[i] = a;
-    sum += a;
-  }
+  for (int i = 0; i < kV4; ++i) sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float mean = sum / C;
   float sq = 0.f;
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    const int c = lane + 32 * i;
-    if (c < C) { const float d = v[i] - mean; sq += d * d; }
+  for (int i = 0; i < kV4; ++i) {
+    if (lane + 32 * i < C4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      sq += (a * a + b * b) + (c * c + d * d);
+    }
   }
   for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
   const float rstd = rsqrtf(sq / C + eps);
-  const int64_t mofs = mod_group > 0 ? (int64_t)(row / mod_group) * mod_ld : 0;
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    const int c = lane + 32 * i;
-    if (c < C) {
-      float y = (v[i] - mean) * rstd;
-      if (gamma) y = y * gamma[c] + (beta ? beta[c] : 0.f);
-      if (scale) y = y * (1.f + scale[mofs + c]);
-      if (shift) y = y + shift[mofs + c];
-      out[(int64_t)row * ldo + c] = __float2bfloat16(y);
+  for (int i = 0; i < kV4; ++i) {
+    const int c4 = lane + 32 * i;
+    if (c4 < C4) {
+      float y[4] = {(v[i].x - mean) * rstd, (v[i].y - mean) * rstd, (v[i].z - mean) * rstd, (v[i].w - mean) * rstd};
+      const float s4[4] = {sc[i].x, sc[i].y, sc[i].z, sc[i].w};
+      const float h4[4] = {sh[i].x, sh[i].y, sh[i].z, sh[i].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (gamma) y[e] = y[e] * gamma[4 * c4 + e] + (beta ? beta[4 * c4 + e] : 0.f);
+        if (scale) y[e] = y[e] * (1.f + s4[e]);
+        if (shift) y[e] = y[e] + h4[e];
+      }
+      uint2 u;
+      *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(y[0], y[1]);
+      *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(y[2], y[3]);
+      reinterpret_cast<uint2*>(out + (int64_t)row * ldo)[c4] = u;
     }
   }
 }
@@ -273,18 +296,19 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
                              const float* beta, const float* shift, const float* scale, int mod_group,
                              int64_t mod_ld, float eps, void* out, int64_t ldo, void* stream) {
   if (M <= 0 || C <= 0) return M == 0 ? DRS_OK : DRS_ERR_VALUE;
-  if (!x || !out || C > 32 * 64) return DRS_ERR_VALUE;
+  if (!x || !out || C > 128 * 16 || C % 4 || ldx % 4 || ldo % 4 || (mod_group > 0 && mod_ld % 4)) return DRS_ERR_VALUE;
   const int warps = 8;
   dim3 grid((M + warps - 1) / warps);
   cudaStream_t st = (cudaStream_t)stream;
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
-  const int vec = (C + 31) / 32;
-  if (vec <= 16)
-    layernorm_kernel<16><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
-  else if (vec <= 48)
-    layernorm_kernel<48><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
-  else
-    layernorm_kernel<64><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, mod_group, mod_ld, eps, o, ldo);
+  const int v4 = (C / 4 + 31) / 32;
+#define DRS_LN(K) layernorm_kernel<K><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, \
+                                                                  mod_group, mod_ld, eps, o, ldo)
+  if (v4 <= 4) DRS_LN(4);
+  else if (v4 <= 8) DRS_LN(8);
+  else if (v4 <= 12) DRS_LN(12);
+  else DRS_LN(16);
+#undef DRS_LN
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 

@@ -47,6 +47,8 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
         assert colscale.dtype == torch.float32
     if bn == 0:
         bn = pick_bn(M, N)
+    if split == 0:
+        split = pick_split(M, N, K, bn)
     ws = _workspace(x.device, split * M * N) if split > 1 else None
     st = _lib.lib().drs_gemm_bf16_ex(
         x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0), M, N, K,
@@ -63,6 +65,15 @@ def pick_bn(M, N):
         if m_tiles * ((N + bn - 1) // bn) >= 148:
             return bn
     return 64 if m_tiles * ((N + 127) // 128) < 74 else 128
+
+
+def pick_split(M, N, K, bn):
+    """Deterministic split-K when the tile grid leaves most SMs idle (small-M GEMMs)."""
+    tiles = ((M + 127) // 128) * ((N + bn - 1) // bn)
+    kb = (K + 63) // 64
+    if tiles >= 96 or kb < 8 or M > 1024:
+        return 1
+    return max(1, min(kb // 4, 148 // tiles, 8))
 
 
 def layernorm(x, out=None, gamma=None, beta=None, shift=None, scale=None, eps=1e-6, mod_group=0):

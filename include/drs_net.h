@@ -32,15 +32,26 @@ int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* 
                   int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
                   int act, int out_f32, float alpha, int bn, int split, float* workspace, void* stream);
 
-/* Same with the extended epilogue used by the transformer blocks:
- *   C = act(alpha*A.B^T + bias) * colscale + residual
- * residual fp32 (res_f32 = 1, the DiT residual stream) or bf16; colscale fp32
- * or NULL (the adaLN-Zero gate): colscale[(row / cs_group) * cs_ld + n] when
- * cs_group > 0 (one gate vector per sample of a token batch), else colscale[n]. */
-int drs_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                     int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
-                     int res_f32, const float* colscale, int cs_group, int64_t cs_ld, int act, int out_f32,
-                     float alpha, int bn, int split, float* workspace, void* stream);
+/* Full-epilogue form:
+ *   C = act(alpha*A.B^T + bias[n] + rowbias[(m / rb_group)*rb_ld + n]) * colscale + residual
+ * residual fp32 (res_f32 = 1, a transformer residual stream) or bf16;
+ * colscale (adaLN-Zero gate) indexed [(m / cs_group)*cs_ld + n] if cs_group > 0
+ * else [n]; rowbias = per-image bias (UNet time-embedding injection). */
+typedef struct drs_gemm_args {
+  const void* A; int64_t lda;
+  const void* B; int64_t ldb;
+  void* C; int64_t ldc;
+  int M, N, K;
+  int act, out_f32;
+  float alpha;
+  const float* bias;
+  const void* residual; int64_t ldr; int res_f32;
+  const float* colscale; int cs_group; int64_t cs_ld;
+  const float* rowbias; int rb_group; int64_t rb_ld;
+  int bn, split;
+  float* workspace;
+} drs_gemm_args;
+int drs_gemm(const drs_gemm_args* args, void* stream);
 
 /* out[m, :] = LN(x[m, :]) (*gamma + beta) (*(1 + scale) + shift) -> bf16.
  * x fp32 (x_f32 = 1) or bf16; gamma/beta fp32 [C] or NULL; shift/scale fp32
@@ -61,6 +72,19 @@ int drs_timestep_embedding(const float* t, int n, int dim, float max_period, voi
 int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out_bf16, void* stream);
 int drs_unpatchify(const float* tok, int Cout, int Ckeep, int H, int W, int p, float* out, void* stream);
 int drs_silu_cast(const float* x, int64_t n, void* out_bf16, void* stream);
+int drs_cast_f32_bf16(const float* x, int64_t n, void* out_bf16, void* stream);
+
+/* UNet helpers (NHWC bf16 activations) */
+/* A[(n,oy,ox), (ky,kx,c)] for a ks x ks conv over the channel concat [x1 | x2],
+ * stride/pad, nearest-upsampled input when up = 2.  C1, C2 multiples of 8. */
+int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N, int H, int W, int ks, int stride,
+               int pad, int up, void* out, void* stream);
+/* GroupNorm(G) + affine (+ SiLU) over NHWC, one CTA per (image, group). */
+int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma, const float* beta,
+                  float eps, int silu, void* out, void* stream);
+int drs_latent_to_nhwc(const void* x, int x_f64, int C, int HW, int Cpad, void* out, void* stream);
+/* eps (C,H,W) fp32 = u + g (c - u) from NHWC fp32 rows [uncond | cond] (pair = 1) */
+int drs_cfg_combine(const float* y, int64_t ld, int HW, int C, float g, int pair, float* eps, void* stream);
 
 #ifdef __cplusplus
 }

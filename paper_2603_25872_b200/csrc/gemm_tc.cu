@@ -46,6 +46,9 @@ struct EpiParams {
   const float* colscale;    // per-column scale applied after act (adaLN gate) or null:
   int cs_group;             //   colscale[(row / cs_group) * cs_ld + n] if cs_group > 0, else colscale[n]
   int64_t cs_ld;
+  const float* rowbias;     // per-row-group bias added before act (UNet time embedding) or null:
+  int rb_group;             //   rowbias[(row / rb_group) * rb_ld + n]
+  int64_t rb_ld;
   float alpha;
   int act;                  // DRS_ACT_*
   int out_f32;              // 1: fp32 output, 0: bf16
@@ -55,11 +58,13 @@ struct EpiParams {
 // Apply the epilogue to 32 consecutive accumulator columns n0..n0+31 of `row`.
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
   if (row >= M) return;
+  const float* rb = p.rowbias ? p.rowbias + (int64_t)(row / p.rb_group) * p.rb_ld : nullptr;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int n = n0 + j;
     float x = v[j] * p.alpha;
     if (p.bias && n < N) x += __ldg(p.bias + n);
+    if (rb && n < N) x += __ldg(rb + n);
     v[j] = x;
   }
   if (p.act == DRS_ACT_GEGLU) {                // interleaved (value, gate) pairs -> N/2 outputs
@@ -379,31 +384,24 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
 
 }  // namespace drs
 
-extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                             int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
-                             int act, int out_f32, float alpha, int bn, int split, float* workspace,
-                             void* stream) {
-  return drs_gemm_bf16_ex(A, lda, B, ldb, C, ldc, M, N, K, bias, residual, ldr, 0, nullptr, 0, 0, act, out_f32,
-                          alpha, bn, split, workspace, stream);
-}
-
-extern "C" int drs_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                                int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
-                                int res_f32, const float* colscale, int cs_group, int64_t cs_ld, int act,
-                                int out_f32, float alpha, int bn, int split, float* workspace, void* stream) {
+extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   using namespace drs;
+  if (!g) return DRS_ERR_VALUE;
+  const int M = g->M, N = g->N, K = g->K;
   if (M <= 0 || N <= 0 || K <= 0) return (M == 0 || N == 0) ? DRS_OK : DRS_ERR_VALUE;
-  if (!A || !B || !C) return DRS_ERR_VALUE;
-  if ((K % 8) || (lda % 8) || (ldb % 8)) return DRS_ERR_VALUE;          // TMA: 16-byte row strides
-  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return DRS_ERR_VALUE;
-  if (act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
-  if (bn == 0) bn = 128;
+  if (!g->A || !g->B || !g->C) return DRS_ERR_VALUE;
+  if ((K % 8) || (g->lda % 8) || (g->ldb % 8)) return DRS_ERR_VALUE;     // TMA: 16-byte row strides
+  if ((reinterpret_cast<uintptr_t>(g->A) & 15) || (reinterpret_cast<uintptr_t>(g->B) & 15)) return DRS_ERR_VALUE;
+  if (g->act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
+  if (g->rowbias && g->rb_group <= 0) return DRS_ERR_VALUE;
+  int bn = g->bn ? g->bn : 128;
   if (bn != 64 && bn != 128 && bn != 256) return DRS_ERR_VALUE;
-  if (split < 1) split = 1;
-  if (split > 1 && !workspace) return DRS_ERR_VALUE;
+  const int split = g->split < 1 ? 1 : g->split;
+  if (split > 1 && !g->workspace) return DRS_ERR_VALUE;
   CUtensorMap ta, tb;
-  if (!make_tmap(&ta, A, M, K, lda, kBM) || !make_tmap(&tb, B, N, K, ldb, bn)) return DRS_ERR_CUDA;
-  EpiParams ep{C, ldc, bias, residual, ldr, res_f32, colscale, cs_group, cs_ld, alpha, act, out_f32, workspace};
+  if (!make_tmap(&ta, g->A, M, K, g->lda, kBM) || !make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
+  EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, g->workspace};
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, st);
@@ -413,4 +411,15 @@ extern "C" int drs_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64
   const int64_t threads = (int64_t)M * ((N + 31) / 32);
   gemm_reduce_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(M, N, split, ep);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                             int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
+                             int act, int out_f32, float alpha, int bn, int split, float* workspace,
+                             void* stream) {
+  drs_gemm_args g = {};
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc; g.M = M; g.N = N; g.K = K;
+  g.bias = bias; g.residual = residual; g.ldr = ldr; g.act = act; g.out_f32 = out_f32; g.alpha = alpha;
+  g.bn = bn; g.split = split; g.workspace = workspace;
+  return drs_gemm(&g, stream);
 }

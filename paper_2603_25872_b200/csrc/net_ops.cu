@@ -283,9 +283,128 @@ __global__ void unpatchify_kernel(const float* __restrict__ tok, int Cout, int C
   out[i] = tok[(int64_t)t * (p * p * Cout) + f];
 }
 
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    uint2 u;
+    *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(v.x, v.y);
+    *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<uint2*>(out + i) = u;
+  } else {
+    for (int64_t j = i; j < n; ++j) out[j] = __float2bfloat16(x[j]);
+  }
+}
+
 __global__ void silu_cast_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { const float a = x[i]; out[i] = __float2bfloat16(a / (1.f + __expf(-a))); }
+}
+
+// ------------------------------------------------------------- UNet ops ----
+// im2col over NHWC bf16 for 1x1 / 3x3 convs: row (n, oy, ox), column
+// (ky, kx, c) with c over the channel concat [x1 | x2] (UNet skip connections);
+// `up` = 2 reads a nearest-upsampled input (Upsample2D folded in); zero padding.
+// One thread per 8-channel (16-byte) chunk.
+__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x1, int C1, const __nv_bfloat16* __restrict__ x2,
+                              int C2, int N, int H, int W, int ks, int stride, int pad, int up, int Ho, int Wo,
+                              __nv_bfloat16* __restrict__ out) {
+  const int C = C1 + C2, C8 = C / 8;
+  const int64_t total = (int64_t)N * Ho * Wo * ks * ks * C8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int c8 = (int)(i % C8);
+  int64_t r = i / C8;
+  const int tap = (int)(r % (ks * ks));
+  r /= (ks * ks);
+  const int ox = (int)(r % Wo);
+  const int oy = (int)((r / Wo) % Ho);
+  const int n = (int)(r / ((int64_t)Wo * Ho));
+  const int ky = tap / ks, kx = tap % ks;
+  const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;   // in upsampled coordinates
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (iy >= 0 && ix >= 0 && iy < H * up && ix < W * up) {
+    const int sy = iy / up, sx = ix / up;
+    const int64_t pix = ((int64_t)n * H + sy) * W + sx;
+    const int c = c8 * 8;
+    v = c < C1 ? *reinterpret_cast<const uint4*>(x1 + pix * C1 + c)
+               : *reinterpret_cast<const uint4*>(x2 + pix * C2 + (c - C1));
+  }
+  *reinterpret_cast<uint4*>(out + i * 8) = v;
+}
+
+// GroupNorm over NHWC (bf16 or fp32 in) with affine and optional SiLU -> bf16.
+// One CTA per (image, group); pass 1 sums (fp32), pass 2 normalises.
+__global__ void groupnorm_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
+                                 const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                                 int silu, __nv_bfloat16* __restrict__ out) {
+  const int n = blockIdx.x / G, g = blockIdx.x % G;
+  const int cg = C / G;
+  const int64_t base = (int64_t)n * HW * C + (int64_t)g * cg;
+  const int total = HW * cg;
+  auto ld = [&](int idx) -> float {
+    const int p = idx / cg, c = idx % cg;
+    const int64_t off = base + (int64_t)p * C + c;
+    return x_f32 ? static_cast<const float*>(x)[off] : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[off]);
+  };
+  float s = 0.f, ss = 0.f;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const float v = ld(idx);
+    s += v;
+    ss += v * v;
+  }
+  __shared__ float red[2][32];
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { red[0][warp] = s; red[1][warp] = ss; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? red[0][lane] : 0.f;
+    ss = lane < nw ? red[1][lane] : 0.f;
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if (lane == 0) { red[0][0] = s; red[1][0] = ss; }
+  }
+  __syncthreads();
+  const float mean = red[0][0] / total;
+  const float var = fmaxf(red[1][0] / total - mean * mean, 0.f);
+  const float rstd = rsqrtf(var + eps);
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int p = idx / cg, c = idx % cg;
+    const int ch = g * cg + c;
+    float v = (ld(idx) - mean) * rstd * gamma[ch] + beta[ch];
+    if (silu) v = v / (1.f + __expf(-v));
+    out[base + (int64_t)p * C + c] = __float2bfloat16(v);
+  }
+}
+
+// latent (C, H, W) fp64/fp32 -> NHWC bf16 with Cpad channels (zeros beyond C)
+__global__ void latent_to_nhwc_kernel(const void* __restrict__ x, int x_f64, int C, int HW, int Cpad,
+                                      __nv_bfloat16* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= HW * Cpad) return;
+  const int p = i / Cpad, c = i % Cpad;
+  float v = 0.f;
+  if (c < C) v = x_f64 ? (float)static_cast<const double*>(x)[(int64_t)c * HW + p]
+                       : static_cast<const float*>(x)[(int64_t)c * HW + p];
+  out[i] = __float2bfloat16(v);
+}
+
+// classifier-free guidance: rows [0, HW) = uncond, [HW, 2HW) = cond (NHWC fp32, ld
+// columns); eps (C, H, W) = u + g (c - u).  g == 1 or ld == 0: single image.
+__global__ void cfg_combine_kernel(const float* __restrict__ y, int64_t ld, int HW, int C, float g, int pair,
+                                   float* __restrict__ eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C * HW) return;
+  const int c = i / HW, p = i % HW;
+  const float u = y[(int64_t)p * ld + c];
+  eps[i] = pair ? u + g * (y[(int64_t)(HW + p) * ld + c] - u) : u;
 }
 
 }  // namespace drs
@@ -366,6 +485,47 @@ extern "C" int drs_silu_cast(const float* x, int64_t n, void* out, void* stream)
   if (n < 0) return DRS_ERR_VALUE;
   if (n == 0) return DRS_OK;
   silu_cast_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      x, n, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N, int H, int W, int ks, int stride,
+                          int pad, int up, void* out, void* stream) {
+  if ((C1 % 8) || (C2 % 8) || (C2 && !x2) || ks < 1 || stride < 1 || up < 1) return DRS_ERR_VALUE;
+  const int Ho = (H * up + 2 * pad - ks) / stride + 1, Wo = (W * up + 2 * pad - ks) / stride + 1;
+  const int64_t total = (int64_t)N * Ho * Wo * ks * ks * ((C1 + C2) / 8);
+  im2col_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const __nv_bfloat16*>(x1), C1, static_cast<const __nv_bfloat16*>(x2), C2, N, H, W, ks, stride, pad,
+      up, Ho, Wo, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma,
+                             const float* beta, float eps, int silu, void* out, void* stream) {
+  if (N <= 0 || HW <= 0 || G <= 0 || C % G || !gamma || !beta) return DRS_ERR_VALUE;
+  groupnorm_kernel<<<N * G, 512, 0, (cudaStream_t)stream>>>(x, x_f32, HW, C, G, gamma, beta, eps, silu,
+                                                            static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_latent_to_nhwc(const void* x, int x_f64, int C, int HW, int Cpad, void* out, void* stream) {
+  if (Cpad < C) return DRS_ERR_VALUE;
+  latent_to_nhwc_kernel<<<(HW * Cpad + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      x, x_f64, C, HW, Cpad, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_cfg_combine(const float* y, int64_t ld, int HW, int C, float g, int pair, float* eps,
+                               void* stream) {
+  cfg_combine_kernel<<<(C * HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(y, ld, HW, C, g, pair, eps);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_cast_f32_bf16(const float* x, int64_t n, void* out, void* stream) {
+  if (n < 0 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 7)) return DRS_ERR_VALUE;
+  if (n == 0) return DRS_OK;
+  const int64_t th = (n + 3) / 4;
+  cast_f32_bf16_kernel<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       x, n, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

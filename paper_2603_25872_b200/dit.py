@@ -15,7 +15,7 @@ Per forward (B images, M = 256 B tokens), all on device, no host sync:
   per block: LN+modulate -> GEMM qkv -> attention -> GEMM proj (*gate, +h)
              LN+modulate -> GEMM fc1 (tanh-GELU) -> GEMM fc2 (*gate, +h)
   final: LN+modulate -> GEMM -> unpatchify -> eps (first 4 channels, fp32)
-The 28 x 4 GEMMs run on the tcgen05 kernel (drs_gemm_bf16_ex); the adaLN
+The 28 x 4 GEMMs run on the tcgen05 kernel (drs_gemm); the adaLN
 gate multiply and the residual add are fused into their epilogues.
 """
 

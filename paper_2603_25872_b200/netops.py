@@ -27,9 +27,10 @@ def _ptr(t):
 
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
-           bn=0, split=1, colscale=None, cs_group=0):
-    """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias) * colscale (+ residual);
-    N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out)."""
+           bn=0, split=1, colscale=None, cs_group=0, rowbias=None, rb_group=0):
+    """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
+    N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
+    rowbias (n_groups, >=N) views indexed by row // group."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
     M, K = x.shape
     N = w.shape[0]
@@ -37,24 +38,31 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     n_out = N // 2 if act == "geglu" else N
     if out is None:
         out = torch.empty(M, n_out, dtype=out_dtype, device=x.device)
-    res_f32 = 0
-    if residual is not None:
-        assert residual.stride(1) == 1 and residual.dtype in (torch.bfloat16, torch.float32)
-        res_f32 = 1 if residual.dtype == torch.float32 else 0
+    g = _lib.DrsGemmArgs()
+    g.A, g.lda, g.B, g.ldb, g.C, g.ldc = x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0)
+    g.M, g.N, g.K = M, N, K
+    g.act, g.out_f32, g.alpha = ACT[act], 1 if out.dtype == torch.float32 else 0, float(alpha)
     if bias is not None:
         assert bias.dtype == torch.float32
+        g.bias = bias.data_ptr()
+    if residual is not None:
+        assert residual.stride(1) == 1 and residual.dtype in (torch.bfloat16, torch.float32)
+        g.residual, g.ldr, g.res_f32 = residual.data_ptr(), residual.stride(0), int(residual.dtype == torch.float32)
     if colscale is not None:
         assert colscale.dtype == torch.float32
+        g.colscale, g.cs_group = colscale.data_ptr(), cs_group
+        g.cs_ld = colscale.stride(0) if colscale.dim() == 2 else 0
+    if rowbias is not None:
+        assert rowbias.dtype == torch.float32 and rb_group > 0
+        g.rowbias, g.rb_group, g.rb_ld = rowbias.data_ptr(), rb_group, rowbias.stride(0)
     if bn == 0:
         bn = pick_bn(M, N)
     if split == 0:
         split = pick_split(M, N, K, bn)
-    ws = _workspace(x.device, split * M * N) if split > 1 else None
-    st = _lib.lib().drs_gemm_bf16_ex(
-        x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0), M, N, K,
-        _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0, res_f32, _ptr(colscale),
-        cs_group, colscale.stride(0) if (colscale is not None and colscale.dim() == 2) else 0, ACT[act], 1 if out.dtype == torch.float32 else 0, float(alpha), bn, split, _ptr(ws), _lib.stream_ptr())
-    _lib.check(st, "drs_gemm_bf16")
+    g.bn, g.split = bn, split
+    if split > 1:
+        g.workspace = _workspace(x.device, split * M * N).data_ptr()
+    _lib.check(_lib.lib().drs_gemm(_lib.ctypes.byref(g), _lib.stream_ptr()), "drs_gemm")
     return out
 
 
@@ -120,4 +128,35 @@ def unpatchify(tok, c_out, c_keep, H, W, p, out):
 def silu_cast(x, out):
     _lib.check(_lib.lib().drs_silu_cast(x.data_ptr(), x.numel(), out.data_ptr(), _lib.stream_ptr()),
                "drs_silu_cast")
+    return out
+
+
+def im2col(x1, C1, x2, C2, N, H, W, ks, stride, pad, up, out):
+    _lib.check(_lib.lib().drs_im2col(x1.data_ptr(), C1, _ptr(x2), C2, N, H, W, ks, stride, pad, up,
+                                     out.data_ptr(), _lib.stream_ptr()), "drs_im2col")
+    return out
+
+
+def groupnorm(x, N, HW, C, G, gamma, beta, out, eps=1e-5, silu=False):
+    _lib.check(_lib.lib().drs_groupnorm(x.data_ptr(), 1 if x.dtype == torch.float32 else 0, N, HW, C, G,
+                                        gamma.data_ptr(), beta.data_ptr(), float(eps), 1 if silu else 0,
+                                        out.data_ptr(), _lib.stream_ptr()), "drs_groupnorm")
+    return out
+
+
+def latent_to_nhwc(x, C, HW, Cpad, out):
+    _lib.check(_lib.lib().drs_latent_to_nhwc(x.data_ptr(), 1 if x.dtype == torch.float64 else 0, C, HW, Cpad,
+                                             out.data_ptr(), _lib.stream_ptr()), "drs_latent_to_nhwc")
+    return out
+
+
+def cfg_combine(y, HW, C, g, pair, eps_out):
+    _lib.check(_lib.lib().drs_cfg_combine(y.data_ptr(), y.stride(0), HW, C, float(g), 1 if pair else 0,
+                                          eps_out.data_ptr(), _lib.stream_ptr()), "drs_cfg_combine")
+    return eps_out
+
+
+def cast_f32_bf16(x, out):
+    _lib.check(_lib.lib().drs_cast_f32_bf16(x.data_ptr(), x.numel(), out.data_ptr(), _lib.stream_ptr()),
+               "drs_cast_f32_bf16")
     return out

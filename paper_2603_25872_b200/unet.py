@@ -1,0 +1,318 @@
+"""SD1.5- and SDXL-shaped conditional UNets (BASELINE configs C3, C5) on this
+package's kernels, random-init (no checkpoints offline).
+
+Layout: NHWC bf16 activations, so every 1x1 conv / linear is a GEMM over
+(pixels, channels) and every 3x3 conv is im2col (drs_im2col, which also
+folds in the skip-connection concat and the nearest-2x upsample) followed by
+the tcgen05 GEMM (drs_gemm) with bias / time-embedding (per-image row bias) /
+residual fused into the epilogue.  Classifier-free guidance runs the
+(uncond, cond) pair as one batch-2 forward; eps = u + g (c - u) is formed in
+the output kernel (drs_cfg_combine).  Cross-attention K/V of the fixed
+random text context are computed once at construction.
+
+Blocks (diffusers UNet2DConditionModel semantics): ResnetBlock2D
+(GN+SiLU -> conv3x3 (+temb) -> GN+SiLU -> conv3x3, 1x1 shortcut),
+Transformer2DModel (GN -> proj_in -> depth x [LN self-attn, LN cross-attn,
+LN GEGLU FF] -> proj_out + residual), Downsample2D (conv3x3 stride 2),
+Upsample2D (nearest 2x + conv3x3).
+"""
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import netops as ops
+
+
+@dataclass(frozen=True)
+class UNetConfig:
+    name: str = "sd15"
+    in_ch: int = 4
+    out_ch: int = 4
+    size: int = 64
+    channels: tuple = (320, 640, 1280, 1280)
+    layers_per_block: int = 2
+    tx_depth: tuple = (1, 1, 1, 0)        # transformer layers per attention, per down level
+    mid_tx_depth: int = 1
+    heads: int = 8                        # SD1.5: fixed 8 heads
+    head_dim: int = 0                     # SDXL: fixed 64-dim heads (heads = c / 64)
+    ctx_dim: int = 768
+    ctx_len: int = 77
+    add_embed_dim: int = 0                # SDXL: 2816 (pooled 1280 + 6 x 256 time ids)
+    groups: int = 32
+    temb_dim: int = 1280
+
+    def n_heads(self, c):
+        return c // self.head_dim if self.head_dim else self.heads
+
+
+def sd15_config(size=64):
+    return UNetConfig(size=size)
+
+
+def sdxl_config(size=128):
+    return UNetConfig(name="sdxl", size=size, channels=(320, 640, 1280), tx_depth=(0, 2, 10), mid_tx_depth=10,
+                      heads=0, head_dim=64, ctx_dim=2048, add_embed_dim=2816)
+
+
+class _Init:
+    def __init__(self, device, seed, std=0.02):
+        self.g = torch.Generator(device=device).manual_seed(seed)
+        self.device, self.std = device, std
+
+    def mat(self, n, k):
+        return (torch.randn(n, k, generator=self.g, device=self.device) * self.std).to(torch.bfloat16)
+
+    def vec(self, n, std=None):
+        return torch.randn(n, generator=self.g, device=self.device) * (self.std if std is None else std)
+
+    def gn(self, c):
+        return (1.0 + self.vec(c, 0.1), self.vec(c, 0.1))
+
+
+class UNet:
+    def __init__(self, cfg: UNetConfig = UNetConfig(), device="cuda", seed: int = 0, max_batch: int = 1,
+                 cfg_scale: float = 7.5):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.cfg_scale = cfg_scale
+        self.max_batch = max_batch                   # images per forward (each is a CFG pair)
+        self.latent_numel = cfg.in_ch * cfg.size * cfg.size
+        I = _Init(self.device, seed)
+        c0, T = cfg.channels[0], cfg.temb_dim
+        self.p = p = {}
+        p["conv_in"] = (I.mat(c0, 9 * 64), I.vec(c0))                # input padded to 64 channels
+        p["t1"] = (I.mat(T, c0), I.vec(T))
+        p["t2"] = (I.mat(T, T), I.vec(T))
+        if cfg.add_embed_dim:
+            p["a1"] = (I.mat(T, cfg.add_embed_dim), I.vec(T))
+            p["a2"] = (I.mat(T, T), I.vec(T))
+        # fixed random text context: [uncond, cond] x ctx_len x ctx_dim (+ SDXL pooled / time ids)
+        self.ctx = torch.randn(2 * cfg.ctx_len, cfg.ctx_dim, generator=I.g, device=self.device).to(torch.bfloat16)
+        if cfg.add_embed_dim:
+            self.add_in = torch.randn(2, cfg.add_embed_dim, generator=I.g, device=self.device).to(torch.bfloat16)
+        self.blocks = []          # ordered description of the network (built once)
+        self.temb_slices = []     # (offset, c) of every resblock's time projection
+        self._temb_w, self._temb_b = [], []
+        skips = [c0]
+        c = c0
+        nlev = len(cfg.channels)
+        for lev, co in enumerate(cfg.channels):
+            for _ in range(cfg.layers_per_block):
+                self.blocks.append(("res", self._res(I, c, 0, co), lev))
+                c = co
+                if cfg.tx_depth[lev]:
+                    self.blocks.append(("tx", self._tx(I, c, cfg.tx_depth[lev]), lev))
+                self.blocks.append(("push", None, lev))
+                skips.append(c)
+            if lev < nlev - 1:
+                self.blocks.append(("down", (I.mat(c, 9 * c), I.vec(c)), lev))
+                self.blocks.append(("push", None, lev))
+                skips.append(c)
+        self.blocks.append(("res", self._res(I, c, 0, c), nlev - 1))
+        if cfg.mid_tx_depth:
+            self.blocks.append(("tx", self._tx(I, c, cfg.mid_tx_depth), nlev - 1))
+        self.blocks.append(("res", self._res(I, c, 0, c), nlev - 1))
+        for i, co in enumerate(reversed(cfg.channels)):
+            lev = nlev - 1 - i
+            depth = cfg.tx_depth[lev]
+            for _ in range(cfg.layers_per_block + 1):
+                cs = skips.pop()
+                self.blocks.append(("res", self._res(I, c, cs, co), lev))
+                c = co
+                if depth:
+                    self.blocks.append(("tx", self._tx(I, c, depth), lev))
+            if lev > 0:
+                self.blocks.append(("up", (I.mat(c, 9 * c), I.vec(c)), lev))
+        p["gn_out"] = I.gn(c)
+        p["conv_out"] = (I.mat(cfg.out_ch, 9 * c), I.vec(cfg.out_ch))
+        self.temb_w = torch.cat(self._temb_w, 0).contiguous()
+        self.temb_b = torch.cat(self._temb_b, 0).contiguous()
+        self._buf = {}
+        self.flops = 0.0
+        self._count = True
+
+    # ---------------------------------------------------------------- params ---
+    def _res(self, I, c1, c2, co):
+        cin = c1 + c2
+        off = sum(w.shape[0] for w in self._temb_w)
+        self._temb_w.append(I.mat(co, self.cfg.temb_dim))
+        self._temb_b.append(I.vec(co))
+        return dict(c1=c1, c2=c2, co=co, gn1=I.gn(cin), conv1=(I.mat(co, 9 * cin), I.vec(co)), gn2=I.gn(co),
+                    conv2=(I.mat(co, 9 * co), I.vec(co)), temb_off=off,
+                    sc=(I.mat(co, cin), I.vec(co)) if cin != co else None)
+
+    def _tx(self, I, c, depth):
+        cfg = self.cfg
+        layers = []
+        for _ in range(depth):
+            wk = I.mat(c, cfg.ctx_dim)
+            wv = I.mat(c, cfg.ctx_dim)
+            kv = ops.linear(self.ctx, torch.cat([wk, wv], 0).contiguous())       # (2*ctx_len, 2c), fixed context
+            layers.append(dict(ln1=I.gn(c), qkv=I.mat(3 * c, c), o1=(I.mat(c, c), I.vec(c)), ln2=I.gn(c),
+                               q2=I.mat(c, c), wk=wk, wv=wv, kv=kv, o2=(I.mat(c, c), I.vec(c)), ln3=I.gn(c),
+                               ff1=(I.mat(8 * c, c), I.vec(8 * c)), ff2=(I.mat(c, 4 * c), I.vec(c))))
+        return dict(c=c, gn=I.gn(c), pin=(I.mat(c, c), I.vec(c)), layers=layers, pout=(I.mat(c, c), I.vec(c)))
+
+    # --------------------------------------------------------------- buffers ---
+    def buf(self, tag, shape, dtype=torch.bfloat16):
+        key = (tag, tuple(shape), dtype)
+        b = self._buf.get(key)
+        if b is None:
+            b = torch.empty(shape, dtype=dtype, device=self.device)
+            self._buf[key] = b
+        return b
+
+    def _lin(self, x, w, **kw):
+        if self._count:
+            self.flops += 2.0 * x.shape[0] * w.shape[0] * w.shape[1]
+        return ops.linear(x, w, **kw)
+
+    def _attn(self, q, k, v, out, B, H, Lq, Lk, d):
+        if self._count:
+            self.flops += 4.0 * B * H * Lq * Lk * d
+        return ops.attention(q, k, v, out, B, H, Lq, Lk, d)
+
+    def _conv3(self, x1, c1, x2, c2, N, H, W, wb, stride=1, up=1, **kw):
+        Ho = (H * up + 2 - 3) // stride + 1
+        Wo = (W * up + 2 - 3) // stride + 1
+        A = self.buf("im2col", (N * Ho * Wo, 9 * (c1 + c2)))
+        ops.im2col(x1, c1, x2, c2, N, H, W, 3, stride, 1, up, A)
+        return self._lin(A, wb[0], bias=wb[1], **kw), Ho, Wo
+
+    # ---------------------------------------------------------------- blocks ---
+    def _resblock(self, r, x, skip, N, H, W, temb_all):
+        c1, c2, co = r["c1"], r["c2"], r["co"]
+        HW = H * W
+        if c2:
+            cat = self.buf(f"cat{c1 + c2}_{HW}", (N * HW, c1 + c2))
+            ops.im2col(x, c1, skip, c2, N, H, W, 1, 1, 0, 1, cat)
+            x = cat
+        cin = c1 + c2
+        hn = self.buf(f"gn{cin}_{HW}", (N * HW, cin))
+        ops.groupnorm(x, N, HW, cin, self.cfg.groups, r["gn1"][0], r["gn1"][1], hn, eps=1e-5, silu=True)
+        h1 = self.buf(f"r1_{co}_{HW}", (N * HW, co))
+        tb = temb_all[:, r["temb_off"]:r["temb_off"] + co]
+        self._conv3(hn, cin, None, 0, N, H, W, r["conv1"], out=h1, rowbias=tb, rb_group=HW)
+        hn2 = self.buf(f"gn{co}_{HW}", (N * HW, co))
+        ops.groupnorm(h1, N, HW, co, self.cfg.groups, r["gn2"][0], r["gn2"][1], hn2, eps=1e-5, silu=True)
+        if r["sc"] is not None:
+            short = self.buf(f"sc{co}_{HW}", (N * HW, co))
+            self._lin(x, r["sc"][0], bias=r["sc"][1], out=short)
+        else:
+            short = x
+        out = self.buf(f"res_out{co}_{HW}", (N * HW, co))
+        self._conv3(hn2, co, None, 0, N, H, W, r["conv2"], out=out, residual=short)
+        return out
+
+    def _transformer(self, t, x, N, H, W):
+        cfg = self.cfg
+        c, HW = t["c"], H * W
+        M = N * HW
+        heads = cfg.n_heads(c)
+        d = c // heads
+        hn = self.buf(f"gn{c}_{HW}", (M, c))
+        ops.groupnorm(x, N, HW, c, cfg.groups, t["gn"][0], t["gn"][1], hn, eps=1e-6, silu=False)
+        s = self.buf(f"txs{c}_{HW}", (M, c), torch.float32)                   # fp32 residual stream
+        self._lin(hn, t["pin"][0], bias=t["pin"][1], out=s)
+        n1 = self.buf(f"txn{c}_{HW}", (M, c))
+        qkv = self.buf(f"qkv{c}_{HW}", (M, 3 * c))
+        att = self.buf(f"att{c}_{HW}", (M, c))
+        ffb = self.buf(f"ff{c}_{HW}", (M, 4 * c))
+        for L in t["layers"]:
+            ops.layernorm(s, out=n1, gamma=L["ln1"][0], beta=L["ln1"][1], eps=1e-5)
+            self._lin(n1, L["qkv"], out=qkv)
+            self._attn(qkv[:, :c], qkv[:, c:2 * c], qkv[:, 2 * c:], att, N, heads, HW, HW, d)
+            self._lin(att, L["o1"][0], bias=L["o1"][1], residual=s, out=s)
+            ops.layernorm(s, out=n1, gamma=L["ln2"][0], beta=L["ln2"][1], eps=1e-5)
+            q = qkv[:, :c]
+            self._lin(n1, L["q2"], out=q)
+            kv = L["kv"]
+            # image n uses context pair member n % 2 (uncond / cond)
+            for n in range(N):
+                j = n % 2
+                self._attn(q[n * HW:(n + 1) * HW], kv[j * cfg.ctx_len:(j + 1) * cfg.ctx_len, :c],
+                           kv[j * cfg.ctx_len:(j + 1) * cfg.ctx_len, c:], att[n * HW:(n + 1) * HW], 1, heads, HW,
+                           cfg.ctx_len, d)
+            self._lin(att, L["o2"][0], bias=L["o2"][1], residual=s, out=s)
+            ops.layernorm(s, out=n1, gamma=L["ln3"][0], beta=L["ln3"][1], eps=1e-5)
+            self._lin(n1, L["ff1"][0], bias=L["ff1"][1], act="geglu", out=ffb)
+            self._lin(ffb, L["ff2"][0], bias=L["ff2"][1], residual=s, out=s)
+        sb = self.buf(f"txsb{c}_{HW}", (M, c))
+        ops.cast_f32_bf16(s, sb)
+        out = self.buf(f"tx_out{c}_{HW}", (M, c))
+        self._lin(sb, t["pout"][0], bias=t["pout"][1], residual=x, out=out)
+        return out
+
+    # --------------------------------------------------------------- forward ---
+    def forward(self, xs, t_dev, B: int, outs=None):
+        """xs: B latents (in_ch*S*S fp64/fp32 CUDA rows); t_dev: (>= B,) fp32 model timesteps.
+        Each image runs as a CFG pair (batch 2B); eps (fp32, in_ch*S*S) written to outs[b]."""
+        cfg, p = self.cfg, self.p
+        S, HW = cfg.size, cfg.size * cfg.size
+        N = 2 * B
+        assert B <= self.max_batch
+        if self._count:
+            self.flops = 0.0
+        x_in = self.buf("x_in", (N * HW, 64))
+        for b, x in enumerate(xs):
+            ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b) * HW:(2 * b + 1) * HW])
+            ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b + 1) * HW:(2 * b + 2) * HW])
+        tpair = self.buf("tpair", (N,), torch.float32)
+        tpair.view(B, 2).copy_(t_dev[:B, None].expand(B, 2))
+        tf = self.buf("tfreq", (N, cfg.channels[0]))
+        ops.timestep_embedding(tpair, cfg.channels[0], tf)
+        th = self.buf("th", (N, cfg.temb_dim))
+        self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
+        temb = self.buf("temb", (N, cfg.temb_dim), torch.float32)
+        if cfg.add_embed_dim:
+            ah = self.buf("ah", (N, cfg.temb_dim))
+            self._lin(self.add_in.repeat(B, 1), p["a1"][0], bias=p["a1"][1], act="silu", out=ah)
+            aemb = self.buf("aemb", (N, cfg.temb_dim), torch.float32)
+            self._lin(ah, p["a2"][0], bias=p["a2"][1], out=aemb)
+            self._lin(th, p["t2"][0], bias=p["t2"][1], residual=aemb, out=temb)
+        else:
+            self._lin(th, p["t2"][0], bias=p["t2"][1], out=temb)
+        temb_act = self.buf("temb_act", (N, cfg.temb_dim))
+        ops.silu_cast(temb, temb_act)
+        temb_all = self.buf("temb_all", (N, self.temb_w.shape[0]), torch.float32)
+        self._lin(temb_act, self.temb_w, bias=self.temb_b, out=temb_all)
+
+        h = self.buf("h_in", (N * HW, cfg.channels[0]))
+        self._conv3(x_in, 64, None, 0, N, S, S, p["conv_in"], out=h)
+        H = W = S
+        cur_c = cfg.channels[0]
+        saved = [self._save(h, 0, H)]
+        for kind, blk, lev in self.blocks:
+            if kind == "res":
+                skip = None
+                if blk["c2"]:
+                    skip, sH = saved.pop()
+                    assert sH == H, (sH, H)
+                h = self._resblock(blk, h, skip, N, H, W, temb_all)
+                cur_c = blk["co"]
+            elif kind == "tx":
+                h = self._transformer(blk, h, N, H, W)
+            elif kind == "push":
+                saved.append(self._save(h, len(saved), H))
+            elif kind == "down":
+                out = self.buf(f"down{cur_c}_{H}", (N * (H // 2) * (W // 2), cur_c))
+                h, H, W = self._conv3(h, cur_c, None, 0, N, H, W, blk, stride=2, out=out)
+            elif kind == "up":
+                out = self.buf(f"up{cur_c}_{H}", (N * 4 * H * W, cur_c))
+                h, H, W = self._conv3(h, cur_c, None, 0, N, H, W, blk, up=2, out=out)
+        hn = self.buf(f"gn_out", (N * HW, cur_c))
+        ops.groupnorm(h, N, HW, cur_c, cfg.groups, p["gn_out"][0], p["gn_out"][1], hn, eps=1e-5, silu=True)
+        y = self.buf("y_out", (N * HW, cfg.out_ch), torch.float32)
+        self._conv3(hn, cur_c, None, 0, N, S, S, p["conv_out"], out=y)
+        for b in range(B):
+            dst = outs[b] if outs is not None else self.buf(f"eps{b}", (self.latent_numel,), torch.float32)
+            ops.cfg_combine(y[2 * b * HW:(2 * b + 2) * HW], HW, cfg.in_ch, self.cfg_scale, True, dst)
+        self._count = False
+        return outs
+
+    def _save(self, h, i, H):
+        """Skip tensors are copied out of the producing block's (reused) output buffer."""
+        s = self.buf(f"skip{i}", tuple(h.shape))
+        s.copy_(h)
+        return s, H

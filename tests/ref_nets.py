@@ -44,3 +44,91 @@ def dit_ref(w, cfg, x, t_model, class_label=0):
     out = F.linear(xn, w.f_w.float(), w.f_b).reshape(B, gs, gs, p, p, cfg.out_ch)
     img = torch.einsum("nhwpqc->nchpwq", out).reshape(B, cfg.out_ch, S, S)
     return img[:, :C]
+
+
+def _conv_w(w, cin, k):
+    """(co, k*k*cin) with K order (ky, kx, c) -> torch (co, cin, k, k)."""
+    return w.float().reshape(w.shape[0], k, k, cin).permute(0, 3, 1, 2)
+
+
+def unet_ref(net, x, t_model):
+    """x: (B, 4, S, S) fp32; every image as a CFG pair; returns eps (B, 4, S, S) fp32."""
+    cfg, p = net.cfg, net.p
+    B = x.shape[0]
+    N = 2 * B
+    xx = x.repeat_interleave(2, dim=0)
+    xx = torch.cat([xx, torch.zeros(N, 64 - cfg.in_ch, cfg.size, cfg.size, device=x.device)], 1)
+    tp = t_model.repeat_interleave(2)
+    half = cfg.channels[0] // 2
+    freqs = torch.exp(-math.log(10000.0) * torch.arange(half, device=x.device, dtype=torch.float32) / half)
+    args = tp[:, None] * freqs[None]
+    tf = torch.cat([torch.cos(args), torch.sin(args)], 1)
+    th = F.silu(F.linear(tf, p["t1"][0].float(), p["t1"][1]))
+    temb = F.linear(th, p["t2"][0].float(), p["t2"][1])
+    if cfg.add_embed_dim:
+        ah = F.silu(F.linear(net.add_in.float().repeat(B, 1), p["a1"][0].float(), p["a1"][1]))
+        temb = temb + F.linear(ah, p["a2"][0].float(), p["a2"][1])
+    temb_all = F.linear(F.silu(temb), net.temb_w.float(), net.temb_b)
+    ctx = net.ctx.float().reshape(2, cfg.ctx_len, cfg.ctx_dim)
+
+    def conv(h, wb, cin, stride=1):
+        return F.conv2d(h, _conv_w(wb[0], cin, 3), wb[1], stride=stride, padding=1)
+
+    def res(r, h, skip):
+        if skip is not None:
+            h = torch.cat([h, skip], 1)
+        cin = h.shape[1]
+        a = F.silu(F.group_norm(h, cfg.groups, r["gn1"][0], r["gn1"][1], eps=1e-5))
+        a = conv(a, r["conv1"], cin) + temb_all[:, r["temb_off"]:r["temb_off"] + r["co"], None, None]
+        a = F.silu(F.group_norm(a, cfg.groups, r["gn2"][0], r["gn2"][1], eps=1e-5))
+        short = h if r["sc"] is None else F.conv2d(h, r["sc"][0].float()[:, :, None, None], r["sc"][1])
+        return conv(a, r["conv2"], r["co"]) + short
+
+    def attn(q, k, v, heads):
+        Bq, Lq, c = q.shape
+        d = c // heads
+        q = q.reshape(Bq, Lq, heads, d).transpose(1, 2)
+        k = k.reshape(Bq, -1, heads, d).transpose(1, 2)
+        v = v.reshape(Bq, -1, heads, d).transpose(1, 2)
+        return (torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(d), -1) @ v).transpose(1, 2).reshape(Bq, Lq, c)
+
+    def tx(tb, h):
+        c = tb["c"]
+        Nn, _, H, W = h.shape
+        heads = cfg.n_heads(c)
+        hn = F.group_norm(h, cfg.groups, tb["gn"][0], tb["gn"][1], eps=1e-6)
+        s = F.linear(hn.permute(0, 2, 3, 1).reshape(Nn, H * W, c), tb["pin"][0].float(), tb["pin"][1])
+        for L in tb["layers"]:
+            n1 = F.layer_norm(s, (c,), L["ln1"][0], L["ln1"][1], eps=1e-5)
+            qkv = F.linear(n1, L["qkv"].float())
+            s = s + F.linear(attn(qkv[..., :c], qkv[..., c:2 * c], qkv[..., 2 * c:], heads), L["o1"][0].float(),
+                             L["o1"][1])
+            n2 = F.layer_norm(s, (c,), L["ln2"][0], L["ln2"][1], eps=1e-5)
+            q = F.linear(n2, L["q2"].float())
+            cx = ctx[torch.arange(Nn, device=x.device) % 2]
+            k = F.linear(cx, L["wk"].float())
+            v = F.linear(cx, L["wv"].float())
+            s = s + F.linear(attn(q, k, v, heads), L["o2"][0].float(), L["o2"][1])
+            n3 = F.layer_norm(s, (c,), L["ln3"][0], L["ln3"][1], eps=1e-5)
+            y = F.linear(n3, L["ff1"][0].float(), L["ff1"][1])
+            s = s + F.linear(y[..., 0::2] * F.gelu(y[..., 1::2]), L["ff2"][0].float(), L["ff2"][1])
+        out = F.linear(s, tb["pout"][0].float(), tb["pout"][1]).reshape(Nn, H, W, c).permute(0, 3, 1, 2)
+        return out + h
+
+    h = conv(xx, p["conv_in"], 64)
+    saved = [h]
+    for kind, blk, _ in net.blocks:
+        if kind == "res":
+            h = res(blk, h, saved.pop() if blk["c2"] else None)
+        elif kind == "tx":
+            h = tx(blk, h)
+        elif kind == "push":
+            saved.append(h)
+        elif kind == "down":
+            h = conv(h, blk, h.shape[1], stride=2)
+        elif kind == "up":
+            h = conv(F.interpolate(h, scale_factor=2, mode="nearest"), blk, h.shape[1])
+    hn = F.silu(F.group_norm(h, cfg.groups, p["gn_out"][0], p["gn_out"][1], eps=1e-5))
+    y = conv(hn, p["conv_out"], h.shape[1])
+    u, c = y[0::2], y[1::2]
+    return u + net.cfg_scale * (c - u)

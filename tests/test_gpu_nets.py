@@ -79,3 +79,26 @@ def test_dit_sampler_end_to_end(cuda):
     seq = P.sample_ddpm(s, den, x_T, stream)
     rel = ((traj.final - seq.final).norm() / seq.final.norm()).item()
     assert rel < 0.5, rel
+
+
+@pytest.mark.parametrize("size", [32, 64])
+@pytest.mark.parametrize("g", [0.0, 1.0])
+def test_sd15_unet_vs_torch_fp32(cuda, size, g):
+    """SD1.5-shaped UNet (CFG pair, random init) vs the fp32 torch reference.
+    g = 0 checks the unconditional branch, g = 1 the conditional one (the
+    production g = 7.5 multiplies the branch difference, and with it the bf16
+    error of a small c - u, by 7.5).  bf16 activations through ~100 layers:
+    rel-L2 of each branch <= 3e-2."""
+    from paper_2603_25872_b200.unet import UNet, sd15_config
+    from ref_nets import unet_ref
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    net = UNet(sd15_config(size), cuda, seed=0, max_batch=1, cfg_scale=g)
+    x = torch.randn(4, size, size, device=cuda, dtype=torch.float64)
+    t = torch.tensor([601.0], device=cuda)
+    out = torch.empty(4 * size * size, device=cuda)
+    net.forward([x.reshape(-1)], t, 1, outs=[out])
+    ref = unet_ref(net, x.float()[None], t)[0]
+    rel = ((out.reshape(4, size, size) - ref).norm() / ref.norm()).item()
+    assert torch.isfinite(out).all() and rel < 3e-2, rel
+    assert net.flops > 0

@@ -192,7 +192,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   const int num_kb_total = (K + kBK - 1) / kBK;
   const int kb_per_split = (num_kb_total + split - 1) / split;
   const int num_tiles = m_tiles * n_tiles * split;
-  constexpr uint32_t kTmemCols = 2 * BN;          // double-buffered accumulator
+  constexpr uint32_t kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);   // 2 x BN, pow2
   constexpr uint32_t kIdesc = tc::idesc_bf16_f32(kBM, BN);
 
   if (warp == 0 && lane == 0) {
@@ -395,7 +395,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (g->act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
   if (g->rowbias && g->rb_group <= 0) return DRS_ERR_VALUE;
   int bn = g->bn ? g->bn : 128;
-  if (bn != 64 && bn != 128 && bn != 256) return DRS_ERR_VALUE;
+  if (bn != 64 && bn != 128 && bn != 160 && bn != 192 && bn != 256) return DRS_ERR_VALUE;
   const int split = g->split < 1 ? 1 : g->split;
   if (split > 1 && !g->workspace) return DRS_ERR_VALUE;
   CUtensorMap ta, tb;
@@ -406,6 +406,8 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   int rc;
   if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, st);
   else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, M, N, K, split, ep, st);
+  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, M, N, K, split, ep, st);
+  else if (bn == 192) rc = launch_gemm<192, 5>(ta, tb, M, N, K, split, ep, st);
   else rc = launch_gemm<256, 4>(ta, tb, M, N, K, split, ep, st);
   if (rc != DRS_OK || split == 1) return rc;
   const int64_t threads = (int64_t)M * ((N + 31) / 32);

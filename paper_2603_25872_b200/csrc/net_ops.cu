@@ -334,22 +334,25 @@ __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x1, int C1, cons
 }
 
 // GroupNorm over NHWC (bf16 or fp32 in) with affine and optional SiLU -> bf16.
-// One CTA per (image, group); pass 1 sums (fp32), pass 2 normalises.
-__global__ void groupnorm_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
-                                 const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-                                 int silu, __nv_bfloat16* __restrict__ out) {
-  const int n = blockIdx.x / G, g = blockIdx.x % G;
-  const int cg = C / G;
+// Pass 1 (gn_stats): grid (N*G, kGnSplit); each CTA sums a fixed pixel slice of
+// one (image, group) and writes (sum, sumsq) partials -- no atomics, so the
+// result is bit-reproducible.  Pass 2 (gn_apply): each CTA reduces the
+// partials of the groups it touches in a fixed order, then normalises a
+// pixel range with 16-byte vector loads.
+constexpr int kGnSplit = 16;
+
+__global__ void gn_stats_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
+                                float2* __restrict__ part) {
+  const int ng = blockIdx.x, sp = blockIdx.y;
+  const int n = ng / G, g = ng % G, cg = C / G;
+  const int p0 = (int)((int64_t)HW * sp / kGnSplit), p1 = (int)((int64_t)HW * (sp + 1) / kGnSplit);
   const int64_t base = (int64_t)n * HW * C + (int64_t)g * cg;
-  const int total = HW * cg;
-  auto ld = [&](int idx) -> float {
-    const int p = idx / cg, c = idx % cg;
-    const int64_t off = base + (int64_t)p * C + c;
-    return x_f32 ? static_cast<const float*>(x)[off] : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[off]);
-  };
+  const int total = (p1 - p0) * cg;
   float s = 0.f, ss = 0.f;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const float v = ld(idx);
+    const int p = p0 + idx / cg, c = idx % cg;
+    const int64_t off = base + (int64_t)p * C + c;
+    const float v = x_f32 ? static_cast<const float*>(x)[off] : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[off]);
     s += v;
     ss += v * v;
   }
@@ -361,26 +364,54 @@ __global__ void groupnorm_kernel(const void* __restrict__ x, int x_f32, int HW, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) { red[0][warp] = s; red[1][warp] = ss; }
   __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    s = lane < nw ? red[0][lane] : 0.f;
-    ss = lane < nw ? red[1][lane] : 0.f;
-    for (int o = 16; o; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    }
-    if (lane == 0) { red[0][0] = s; red[1][0] = ss; }
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; }
+    part[(int64_t)ng * kGnSplit + sp] = make_float2(a, b);
+  }
+}
+
+constexpr int kGnPix = 16;     // pixels per apply CTA
+
+__global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
+                                const float2* __restrict__ part, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, float eps, int silu,
+                                __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float sstat[];                  // [G][2] mean, rstd
+  const int64_t pix0 = (int64_t)blockIdx.x * kGnPix;  // global pixel index (n*HW + p)
+  const int n = (int)(pix0 / HW);
+  const int cg = C / G;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    const float2* pp = part + ((int64_t)n * G + g) * kGnSplit;
+    for (int s2 = 0; s2 < kGnSplit; ++s2) { a += pp[s2].x; b += pp[s2].y; }
+    const float cnt = (float)HW * cg;
+    const float mean = a / cnt;
+    const float var = fmaxf(b / cnt - mean * mean, 0.f);
+    sstat[2 * g] = mean;
+    sstat[2 * g + 1] = rsqrtf(var + eps);
   }
   __syncthreads();
-  const float mean = red[0][0] / total;
-  const float var = fmaxf(red[1][0] / total - mean * mean, 0.f);
-  const float rstd = rsqrtf(var + eps);
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int p = idx / cg, c = idx % cg;
-    const int ch = g * cg + c;
-    float v = (ld(idx) - mean) * rstd * gamma[ch] + beta[ch];
-    if (silu) v = v / (1.f + __expf(-v));
-    out[base + (int64_t)p * C + c] = __float2bfloat16(v);
+  const int C2 = C / 2;
+  const int64_t total = (int64_t)kGnPix * C2;
+  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+    const int64_t pix = pix0 + i / C2;
+    if (pix >= (int64_t)(n + 1) * HW) break;       // CTA never straddles images (HW % kGnPix == 0)
+    const int c = (int)(i % C2) * 2;
+    const int64_t off = pix * C + c;
+    float v0, v1;
+    if (x_f32) {
+      const float2 f = *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off);
+      v0 = f.x; v1 = f.y;
+    } else {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off));
+      v0 = f.x; v1 = f.y;
+    }
+    const int g0 = c / cg, g1 = (c + 1) / cg;
+    v0 = (v0 - sstat[2 * g0]) * sstat[2 * g0 + 1] * gamma[c] + beta[c];
+    v1 = (v1 - sstat[2 * g1]) * sstat[2 * g1 + 1] * gamma[c + 1] + beta[c + 1];
+    if (silu) { v0 = v0 / (1.f + __expf(-v0)); v1 = v1 / (1.f + __expf(-v1)); }
+    *reinterpret_cast<__nv_bfloat162*>(out + off) = __floats2bfloat162_rn(v0, v1);
   }
 }
 
@@ -416,6 +447,8 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
                              int64_t mod_ld, float eps, void* out, int64_t ldo, void* stream) {
   if (M <= 0 || C <= 0) return M == 0 ? DRS_OK : DRS_ERR_VALUE;
   if (!x || !out || C > 128 * 16 || C % 4 || ldx % 4 || ldo % 4 || (mod_group > 0 && mod_ld % 4)) return DRS_ERR_VALUE;
+  auto mis = [](const void* p, uintptr_t a) { return p && (reinterpret_cast<uintptr_t>(p) & (a - 1)); };
+  if (mis(x, x_f32 ? 16 : 8) || mis(out, 8) || mis(shift, 16) || mis(scale, 16)) return DRS_ERR_VALUE;
   const int warps = 8;
   dim3 grid((M + warps - 1) / warps);
   cudaStream_t st = (cudaStream_t)stream;
@@ -501,10 +534,14 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
 }
 
 extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma,
-                             const float* beta, float eps, int silu, void* out, void* stream) {
-  if (N <= 0 || HW <= 0 || G <= 0 || C % G || !gamma || !beta) return DRS_ERR_VALUE;
-  groupnorm_kernel<<<N * G, 512, 0, (cudaStream_t)stream>>>(x, x_f32, HW, C, G, gamma, beta, eps, silu,
-                                                            static_cast<__nv_bfloat16*>(out));
+                             const float* beta, float eps, int silu, void* out, void* workspace, void* stream) {
+  if (N <= 0 || HW <= 0 || G <= 0 || C % G || C % 2 || HW % kGnPix || !gamma || !beta || !workspace)
+    return DRS_ERR_VALUE;
+  cudaStream_t st = (cudaStream_t)stream;
+  float2* part = static_cast<float2*>(workspace);    // N*G*kGnSplit float2
+  gn_stats_kernel<<<dim3(N * G, kGnSplit), 256, 0, st>>>(x, x_f32, HW, C, G, part);
+  gn_apply_kernel<<<(unsigned)((int64_t)N * HW / kGnPix), 256, 2 * G * sizeof(float), st>>>(
+      x, x_f32, HW, C, G, part, gamma, beta, eps, silu, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 

@@ -66,13 +66,22 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     return out
 
 
-def pick_bn(M, N):
-    """Tile width: 256 when there are enough tiles to fill the GPU, else smaller."""
+BN_CHOICES = (64, 128, 160, 192, 256)
+
+
+def pick_bn(M, N, sms=148):
+    """Tile width maximising useful tile area per wave of SMs (UMMA N is any
+    multiple of 16, so 160/192 fit the UNet's 320/640/960 channel counts)."""
     m_tiles = (M + 127) // 128
-    for bn in (256, 128):
-        if m_tiles * ((N + bn - 1) // bn) >= 148:
-            return bn
-    return 64 if m_tiles * ((N + 127) // 128) < 74 else 128
+    best, best_eff = 128, -1.0
+    for bn in BN_CHOICES:
+        tiles = m_tiles * ((N + bn - 1) // bn)
+        waves = (tiles + sms - 1) // sms
+        eff = (M * N) / (waves * sms * 128.0 * bn)
+        eff *= 1.0 + 0.15 * (bn / 256.0)          # larger tiles reuse the A tile more
+        if eff > best_eff:
+            best, best_eff = bn, eff
+    return best
 
 
 def pick_split(M, N, K, bn):
@@ -137,10 +146,18 @@ def im2col(x1, C1, x2, C2, N, H, W, ks, stride, pad, up, out):
     return out
 
 
+_gn_ws = {}
+
+
 def groupnorm(x, N, HW, C, G, gamma, beta, out, eps=1e-5, silu=False):
+    key = (x.device, N * G)
+    ws = _gn_ws.get(key)
+    if ws is None:
+        ws = torch.empty(N * G * 16 * 2, dtype=torch.float32, device=x.device)
+        _gn_ws[key] = ws
     _lib.check(_lib.lib().drs_groupnorm(x.data_ptr(), 1 if x.dtype == torch.float32 else 0, N, HW, C, G,
                                         gamma.data_ptr(), beta.data_ptr(), float(eps), 1 if silu else 0,
-                                        out.data_ptr(), _lib.stream_ptr()), "drs_groupnorm")
+                                        out.data_ptr(), ws.data_ptr(), _lib.stream_ptr()), "drs_groupnorm")
     return out
 
 

@@ -25,7 +25,7 @@ def _ref(x, w, bias, act, res, alpha):
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 1152, 1152), (300, 200, 136), (77, 768, 320),
                                    (1024, 3456, 1152), (4096, 320, 2880), (8, 64, 4608)])
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 128, 160, 192, 256])
 def test_gemm_shapes(cuda, M, N, K, bn):
     from paper_2603_25872_b200.netops import linear
     g = torch.Generator(device=cuda).manual_seed(M * 7 + N)

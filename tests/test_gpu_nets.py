@@ -31,11 +31,13 @@ def test_layernorm_modulate(cuda):
     from paper_2603_25872_b200.netops import layernorm
     x = torch.randn(512, 1152, device=cuda) * 3 + 1
     mod = torch.randn(2, 4000, device=cuda)
-    shift, scale = mod[:, 10:10 + 1152], mod[:, 2000:2000 + 1152]
+    shift, scale = mod[:, 12:12 + 1152], mod[:, 2000:2000 + 1152]
     y = layernorm(x, shift=shift, scale=scale, eps=1e-6, mod_group=256)
     xn = F.layer_norm(x, (1152,), eps=1e-6)
     ref = torch.cat([xn[:256] * (1 + scale[0]) + shift[0], xn[256:] * (1 + scale[1]) + shift[1]])
     assert ((y.float() - ref).abs().max() / ref.abs().max()).item() < 1e-2
+    with pytest.raises(ValueError):                      # misaligned modulation rows are rejected, not faulted
+        layernorm(x, shift=mod[:, 10:10 + 1152], scale=scale, mod_group=256)
     g, b = torch.randn(1152, device=cuda), torch.randn(1152, device=cuda)
     y = layernorm(x.bfloat16(), gamma=g, beta=b, eps=1e-5)
     ref = F.layer_norm(x.bfloat16().float(), (1152,), g, b, eps=1e-5)

@@ -26,6 +26,15 @@ def main():
         net = DiT(cfg, dev, max_batch=max(bs))
         flops1 = cfg.flops_per_image()
         D = 4 * 32 * 32
+    elif a.net in ("sd15", "sdxl"):
+        from paper_2603_25872_b200.unet import UNet, sd15_config, sdxl_config
+        cfgu = sd15_config() if a.net == "sd15" else sdxl_config()
+        bs = [int(b) for b in a.batches.split(",")]
+        net = UNet(cfgu, dev, max_batch=max(bs))
+        D = net.latent_numel
+        xs0 = [torch.randn(D, device=dev, dtype=torch.float64)]
+        net.forward(xs0, torch.full((1,), 500.0, device=dev), 1, [torch.empty(D, device=dev)])
+        flops1 = net.flops
     else:
         raise SystemExit(f"unknown net {a.net}")
     for B in bs:

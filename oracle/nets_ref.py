@@ -1,5 +1,11 @@
-"""Plain PyTorch fp32 references of the denoiser networks (test-only): the
-same random weights (bf16 matrices upcast), the same math, no custom kernels."""
+"""ORACLE -- test infrastructure only (tests/, bench.py CPU legs).
+
+Plain PyTorch fp32 references of the denoiser networks: the same random
+weights (bf16 matrices upcast), the same math, no libdrs kernels.  The
+reference package has no networks (its eps is analytic, skipdiff
+denoiser.py:85-145); BASELINE configs C3-C5 put these shapes behind its
+`evaluate` boundary, and SURVEY 8(d) times them on host cores by injecting
+such a torch-CPU network into the reference sampler."""
 
 import math
 

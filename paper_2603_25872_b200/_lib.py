@@ -170,7 +170,11 @@ _STATUS_EXC = {
 }
 
 
+LAUNCHES = [0]     # libdrs entry points called (== kernel launches issued); read by bench.py
+
+
 def check(status: int, what: str):
+    LAUNCHES[0] += 1
     if status != DRS_OK:
         exc = _STATUS_EXC.get(status, RuntimeError)
         raise exc(f"{what} failed with drs status {status}")

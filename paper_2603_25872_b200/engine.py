@@ -52,8 +52,18 @@ class Comm:
         self.rank, self.size, self.group = rank, size, group
 
     def all_gather_rows(self, gbuf):
+        """In-place all-gather of gbuf[world, per_rank, D]: rank r contributes gbuf[r]."""
         import torch.distributed as dist
         flat = gbuf.view(self.size, -1)
+        if dist.get_backend(self.group) == "gloo":
+            # host-staged path: lets tests run several ranks' kernels on one GPU
+            # (no device-side waits between processes) over a CPU process group
+            parts = [torch.empty_like(flat[0], device="cpu") for _ in range(self.size)]
+            dist.all_gather(parts, flat[self.rank].cpu(), group=self.group)
+            for r, t in enumerate(parts):
+                if r != self.rank:
+                    flat[r].copy_(t)
+            return
         dist.all_gather_into_tensor(flat.view(-1), flat[self.rank], group=self.group)
 
 
@@ -175,6 +185,7 @@ class DeviceRun:
                 pass
         self.n_ops = len(ops_all)
         self.ops_dev = ops_to_device(ops_all, self.device) if ops_all else None
+        self._split_segments()
         self.launch_bytes = [self._algo_bytes(k, p, ops_all) for k, p in self.launches]
 
     def _algo_bytes(self, kind, payload, ops_all):
@@ -260,14 +271,16 @@ class DeviceRun:
             network_eval_into(self.core, a["chunks"])
 
     def enqueue(self, events=None, timers=None):
-        """Issue the whole run on the current stream (capturable when world == 1).
-        Stochastic noise uses the generator of the run's RngStream; the SI
-        table always uses PCG64 (denoiser.py:144).  `events[r]` (start, end)
-        bracket round r; `timers`, if a list, receives (kernel class,
-        algorithmic bytes, start event, end event) for every libdrs launch."""
-        stream = _lib.stream_ptr()
-        L = _lib.lib()
+        """Issue the whole run on the current stream.  Stochastic noise uses the
+        generator of the run's RngStream; the SI table always uses PCG64
+        (denoiser.py:144).  `events[r]` (start, end) bracket round r; `timers`,
+        if a list, receives (kernel class, algorithmic bytes, start event, end
+        event) for every libdrs launch."""
+        for i in range(len(self.segments)):
+            self.enqueue_segment(i, events, timers)
+            self.gather_after(i, events, timers)
 
+    def _timed(self, timers):
         def timed(label, nbytes, fn):
             if timers is None:
                 return fn()
@@ -276,14 +289,23 @@ class DeviceRun:
             fn()
             e1.record()
             timers.append((label, nbytes, e0, e1))
+        return timed
 
-        self.err.zero_()
-        self._enqueue_noise(stream, timed)
-        if self.derive_init:
-            self.traj[0].copy_(self.noise[self.rows[self.init_key]])
-        else:
-            self.traj[0].copy_(self.xin)
-        for (kind, payload), nbytes in zip(self.launches, self.launch_bytes):
+    def enqueue_segment(self, i, events=None, timers=None):
+        """Launches between two eps all-gathers (segment 0 also fills the noise
+        table and stages x_T).  Contains no collective, so it is capturable."""
+        stream = _lib.stream_ptr()
+        L = _lib.lib()
+        timed = self._timed(timers)
+        if i == 0:
+            self.err.zero_()
+            self._enqueue_noise(stream, timed)
+            if self.derive_init:
+                self.traj[0].copy_(self.noise[self.rows[self.init_key]])
+            else:
+                self.traj[0].copy_(self.xin)
+        lo, hi = self.segments[i]
+        for (kind, payload), nbytes in zip(self.launches[lo:hi], self.launch_bytes[lo:hi]):
             if kind == "chain":
                 off, n = payload
                 timed("chain", nbytes, lambda: _lib.check(
@@ -300,10 +322,24 @@ class DeviceRun:
                     timed("eval_" + lowered[0], nbytes, lambda: self._launch_eval(lowered, stream))
                 if events is not None and not self._gathered(rnd):
                     events[rnd][1].record()
-            elif kind == "gather":
-                timed("gather", nbytes, lambda: self.comm.all_gather_rows(self.gbuf))
-                if events is not None:
-                    events[payload][1].record()
+
+    def gather_after(self, i, events=None, timers=None):
+        if i < len(self.gather_rounds):
+            rnd = self.gather_rounds[i]
+            nb = self.prog.world * self.per_rank * self.D * self.gbuf.element_size()
+            self._timed(timers)("gather", nb, lambda: self.comm.all_gather_rows(self.gbuf))
+            if events is not None:
+                events[rnd][1].record()
+
+    def _split_segments(self):
+        self.segments, self.gather_rounds = [], []
+        lo = 0
+        for j, (kind, payload) in enumerate(self.launches):
+            if kind == "gather":
+                self.segments.append((lo, j))
+                self.gather_rounds.append(payload)
+                lo = j + 1
+        self.segments.append((lo, len(self.launches)))
 
     def _gathered(self, rnd):
         return any(k == "gather" and p == rnd for k, p in self.launches)
@@ -342,26 +378,44 @@ class DeviceRun:
                 n += 1 + (1 if self.eval_ms > 0 else 0)
         return n
 
-    def capture(self):
-        """Capture enqueue() into a CUDA graph (single-rank runs only)."""
-        if self.prog.world != 1:
-            raise RuntimeError("multi-rank runs are issued eagerly (NCCL collectives)")
+    def _warm_stream(self):
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
+        return s
+
+    def capture(self):
+        """Capture the run into CUDA graphs: one graph for a single-rank run;
+        one graph per segment between all-gathers for a multi-rank run (the
+        NCCL collectives are issued between segment replays)."""
+        s = self._warm_stream()
         with torch.cuda.stream(s):
-            self.enqueue()                    # warm-up outside capture
+            self.enqueue()                    # warm-up outside capture (allocations, tensor maps)
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            self.enqueue()
-        self.graph = g
-        return g
+        if self.prog.world == 1:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.enqueue()
+            self.graph, self.seg_graphs = g, None
+            return g
+        self.seg_graphs = []
+        for i in range(len(self.segments)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.enqueue_segment(i)
+            self.seg_graphs.append(g)
+        self.graph = None
+        return self.seg_graphs
 
     def replay(self):
-        if self.graph is None:
+        if self.graph is None and not getattr(self, "seg_graphs", None):
             self.capture()
-        self.graph.replay()
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        for i, g in enumerate(self.seg_graphs):
+            g.replay()
+            self.gather_after(i)
 
     def check_err(self):
         from .rng import _check_err

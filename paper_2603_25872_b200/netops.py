@@ -13,6 +13,10 @@ ACT = {None: 0, "none": 0, "gelu_tanh": 1, "silu": 2, "gelu": 3, "geglu": 4}
 
 _ws = {}
 
+# Instrumentation (bench.py): when TIMERS is a list, every GEMM records
+# (flops, start event, end event) on the current stream.
+TIMERS = None
+
 
 def _workspace(device, numel):
     buf = _ws.get(device)
@@ -62,7 +66,13 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     g.bn, g.split = bn, split
     if split > 1:
         g.workspace = _workspace(x.device, split * M * N).data_ptr()
+    if TIMERS is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     _lib.check(_lib.lib().drs_gemm(_lib.ctypes.byref(g), _lib.stream_ptr()), "drs_gemm")
+    if TIMERS is not None:
+        e1.record()
+        TIMERS.append((2.0 * M * N * K, e0, e1))
     return out
 
 
@@ -147,6 +157,10 @@ def im2col(x1, C1, x2, C2, N, H, W, ks, stride, pad, up, out):
 
 
 _gn_ws = {}
+
+# Instrumentation (bench.py): when TIMERS is a list, every GEMM records
+# (flops, start event, end event) on the current stream.
+TIMERS = None
 
 
 def groupnorm(x, N, HW, C, G, gamma, beta, out, eps=1e-5, silu=False):

@@ -35,7 +35,7 @@ class Sampler:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.run = DeviceRun(prog, s, d, dim, dev, generator=generator, comm=comm, derive_init=True)
         self.prog, self.device, self.dim = prog, dev, dim
-        self.use_graph = graph and comm.size == 1
+        self.use_graph = graph
         self.mode, self.devices = mode, devices
         self._seed_pinned = torch.zeros(2, dtype=torch.int64).pin_memory()
 
@@ -61,19 +61,20 @@ class Sampler:
         self._staged.record()
 
     def launch(self):
-        """Enqueue one image on the current stream (graph replay when possible)."""
-        if self.use_graph:
-            key = self.run.derive_init
-            graphs = getattr(self, "_graphs", {})
-            g = graphs.get(key)
-            if g is None:
-                g = self.run.capture()
-                graphs[key] = g
-                self._graphs = graphs
-                self.run.graph = None
-            g.replay()
-        else:
+        """Enqueue one image on the current stream: graph replay (one graph per
+        run on a single rank, one per segment between all-gathers otherwise)."""
+        if not self.use_graph:
             self.run.enqueue()
+            return
+        key = self.run.derive_init
+        graphs = getattr(self, "_graphs", {})
+        if key not in graphs:
+            self.run.graph, self.run.seg_graphs = None, None
+            self.run.capture()
+            graphs[key] = (self.run.graph, self.run.seg_graphs)
+            self._graphs = graphs
+        self.run.graph, self.run.seg_graphs = graphs[key]
+        self.run.replay()
 
     def __call__(self, seed: int, x_T=None, out=None):
         self.stage(seed, x_T)

@@ -148,7 +148,10 @@ class UNet:
         for _ in range(depth):
             wk = I.mat(c, cfg.ctx_dim)
             wv = I.mat(c, cfg.ctx_dim)
-            kv = ops.linear(self.ctx, torch.cat([wk, wv], 0).contiguous())       # (2*ctx_len, 2c), fixed context
+            if self.device.type == "cuda":                                     # fixed context: K/V once
+                kv = ops.linear(self.ctx, torch.cat([wk, wv], 0).contiguous())   # (2*ctx_len, 2c)
+            else:
+                kv = None                                                      # CPU copy: reference use only
             layers.append(dict(ln1=I.gn(c), qkv=I.mat(3 * c, c), o1=(I.mat(c, c), I.vec(c)), ln2=I.gn(c),
                                q2=I.mat(c, c), wk=wk, wv=wv, kv=kv, o2=(I.mat(c, c), I.vec(c)), ln3=I.gn(c),
                                ff1=(I.mat(8 * c, c), I.vec(8 * c)), ff2=(I.mat(c, 4 * c), I.vec(c))))

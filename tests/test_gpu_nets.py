@@ -48,7 +48,7 @@ def test_dit_forward_vs_torch_fp32(cuda):
     """Batched DiT-XL/2 forward (2 images, different t) vs the fp32 torch reference.
     Tolerance: bf16 activations between GEMMs -> rel-L2 of eps <= 3e-2."""
     from paper_2603_25872_b200.dit import DiT, DiTConfig
-    from ref_nets import dit_ref
+    from nets_ref import dit_ref
     cfg = DiTConfig()
     net = DiT(cfg, cuda, seed=0, max_batch=2)
     x = torch.randn(2, 4, 32, 32, device=cuda, dtype=torch.float64)
@@ -92,7 +92,7 @@ def test_sd15_unet_vs_torch_fp32(cuda, size, g):
     error of a small c - u, by 7.5).  bf16 activations through ~100 layers:
     rel-L2 of each branch <= 3e-2."""
     from paper_2603_25872_b200.unet import UNet, sd15_config
-    from ref_nets import unet_ref
+    from nets_ref import unet_ref
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     net = UNet(sd15_config(size), cuda, seed=0, max_batch=1, cfg_scale=g)

@@ -337,8 +337,8 @@ def main():
     if net_cfg:
         gt = netops.TIMERS
         netops.TIMERS = None
-        g_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in gt)
-        g_flops = sum(f for f, _, _ in gt)
+        g_ms = sum(e0.elapsed_time(e1) for _, e0, e1, _ in gt)
+        g_flops = sum(f for f, _, _, _ in gt)
         achieved = g_flops / (g_ms * 1e-3) / 1e12
         peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
         ev_ms = classes.get("eval_net", {"ms": 0.0})["ms"]

@@ -10,8 +10,9 @@
 // MMAs of tile i+1.  Warp roles (192 threads):
 //   warp 0        TMA producer            (one elected lane)
 //   warp 1        TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5    epilogue: tcgen05.ld 32x32b -> registers -> bias / GELU /
-//                 SiLU / GEGLU / residual / alpha -> bf16 or fp32 stores
+//   warps 2..9    epilogue, two warps per TMEM lane quadrant splitting the
+//                 32-column chunks: tcgen05.ld 32x32b -> registers -> bias /
+//                 GELU / SiLU / GEGLU / gate / residual -> bf16 or fp32 stores
 // Grid = min(#tiles, #SMs); each CTA walks tiles t = blockIdx.x, +gridDim.x.
 // Split-K (kSplit > 1): each split accumulates a K range and writes fp32
 // partials; drs_gemm_reduce sums them in a fixed order (deterministic, no
@@ -27,7 +28,8 @@ namespace drs {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;                 // one 128-byte swizzle atom of bf16
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM quadrant)
+constexpr int kEpiWarps = 8;
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -199,7 +201,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     tc::tma_prefetch(&tmap_a);
     tc::tma_prefetch(&tmap_b);
     for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
-    for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], 4); }
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], kEpiWarps); }
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_slot);
@@ -266,8 +268,9 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..9) ----------------
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;              // which 32-column chunks (even / odd) it drains
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int sp = tile % split;
@@ -280,7 +283,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       tc::tc_fence_after();
       const int row = mt * kBM + quad * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int n0 = nt * BN + c * 32;
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);

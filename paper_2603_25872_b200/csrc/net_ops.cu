@@ -347,14 +347,18 @@ __global__ void gn_stats_kernel(const void* __restrict__ x, int x_f32, int HW, i
   const int n = ng / G, g = ng % G, cg = C / G;
   const int p0 = (int)((int64_t)HW * sp / kGnSplit), p1 = (int)((int64_t)HW * (sp + 1) / kGnSplit);
   const int64_t base = (int64_t)n * HW * C + (int64_t)g * cg;
-  const int total = (p1 - p0) * cg;
+  // walk (pixel, channel) incrementally: no division in the loop
+  const int step_p = blockDim.x / cg, step_c = blockDim.x % cg;
+  int p = p0 + threadIdx.x / cg, c = threadIdx.x % cg;
   float s = 0.f, ss = 0.f;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int p = p0 + idx / cg, c = idx % cg;
+  while (p < p1) {
     const int64_t off = base + (int64_t)p * C + c;
     const float v = x_f32 ? static_cast<const float*>(x)[off] : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[off]);
     s += v;
     ss += v * v;
+    c += step_c;
+    p += step_p;
+    if (c >= cg) { c -= cg; ++p; }
   }
   __shared__ float red[2][32];
   for (int o = 16; o; o >>= 1) {
@@ -373,6 +377,9 @@ __global__ void gn_stats_kernel(const void* __restrict__ x, int x_f32, int HW, i
 
 constexpr int kGnPix = 16;     // pixels per apply CTA
 
+// Each thread owns channel pairs (cp, cp + blockDim, ...) and walks the CTA's
+// pixels: group lookups, gamma/beta and the group statistics are hoisted out
+// of the pixel loop.
 __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
                                 const float2* __restrict__ part, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, float eps, int silu,
@@ -393,25 +400,26 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
   }
   __syncthreads();
   const int C2 = C / 2;
-  const int64_t total = (int64_t)kGnPix * C2;
-  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
-    const int64_t pix = pix0 + i / C2;
-    if (pix >= (int64_t)(n + 1) * HW) break;       // CTA never straddles images (HW % kGnPix == 0)
-    const int c = (int)(i % C2) * 2;
-    const int64_t off = pix * C + c;
-    float v0, v1;
-    if (x_f32) {
-      const float2 f = *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off);
-      v0 = f.x; v1 = f.y;
-    } else {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off));
-      v0 = f.x; v1 = f.y;
-    }
+  for (int cp = threadIdx.x; cp < C2; cp += blockDim.x) {
+    const int c = 2 * cp;
     const int g0 = c / cg, g1 = (c + 1) / cg;
-    v0 = (v0 - sstat[2 * g0]) * sstat[2 * g0 + 1] * gamma[c] + beta[c];
-    v1 = (v1 - sstat[2 * g1]) * sstat[2 * g1 + 1] * gamma[c + 1] + beta[c + 1];
-    if (silu) { v0 = v0 / (1.f + __expf(-v0)); v1 = v1 / (1.f + __expf(-v1)); }
-    *reinterpret_cast<__nv_bfloat162*>(out + off) = __floats2bfloat162_rn(v0, v1);
+    const float a0 = sstat[2 * g0 + 1] * gamma[c], a1 = sstat[2 * g1 + 1] * gamma[c + 1];
+    const float b0 = beta[c] - sstat[2 * g0] * a0, b1 = beta[c + 1] - sstat[2 * g1] * a1;
+    for (int pp = 0; pp < kGnPix; ++pp) {
+      const int64_t off = (pix0 + pp) * C + c;
+      float v0, v1;
+      if (x_f32) {
+        const float2 f = *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off);
+        v0 = f.x; v1 = f.y;
+      } else {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off));
+        v0 = f.x; v1 = f.y;
+      }
+      v0 = v0 * a0 + b0;
+      v1 = v1 * a1 + b1;
+      if (silu) { v0 = v0 / (1.f + __expf(-v0)); v1 = v1 / (1.f + __expf(-v1)); }
+      *reinterpret_cast<__nv_bfloat162*>(out + off) = __floats2bfloat162_rn(v0, v1);
+    }
   }
 }
 
@@ -540,7 +548,8 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
   cudaStream_t st = (cudaStream_t)stream;
   float2* part = static_cast<float2*>(workspace);    // N*G*kGnSplit float2
   gn_stats_kernel<<<dim3(N * G, kGnSplit), 256, 0, st>>>(x, x_f32, HW, C, G, part);
-  gn_apply_kernel<<<(unsigned)((int64_t)N * HW / kGnPix), 256, 2 * G * sizeof(float), st>>>(
+  const int c2 = C / 2, thr = c2 >= 256 ? 256 : ((c2 + 31) / 32) * 32;
+  gn_apply_kernel<<<(unsigned)((int64_t)N * HW / kGnPix), thr, 2 * G * sizeof(float), st>>>(
       x, x_f32, HW, C, G, part, gamma, beta, eps, silu, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

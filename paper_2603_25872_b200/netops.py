@@ -31,7 +31,7 @@ def _ptr(t):
 
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
-           bn=0, split=1, colscale=None, cs_group=0, rowbias=None, rb_group=0):
+           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group."""
@@ -72,7 +72,7 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     _lib.check(_lib.lib().drs_gemm(_lib.ctypes.byref(g), _lib.stream_ptr()), "drs_gemm")
     if TIMERS is not None:
         e1.record()
-        TIMERS.append((2.0 * M * N * K, e0, e1))
+        TIMERS.append((2.0 * M * N * K, e0, e1, (M, N, K, bn, split)))
     return out
 
 
@@ -95,12 +95,13 @@ def pick_bn(M, N, sms=148):
 
 
 def pick_split(M, N, K, bn):
-    """Deterministic split-K when the tile grid leaves most SMs idle (small-M GEMMs)."""
+    """Deterministic split-K (fp32 partials + fixed-order reduce) when the tile
+    grid leaves most SMs idle AND each split still has a long K loop."""
     tiles = ((M + 127) // 128) * ((N + bn - 1) // bn)
     kb = (K + 63) // 64
-    if tiles >= 96 or kb < 8 or M > 1024:
+    if tiles > 74 or kb < 48:
         return 1
-    return max(1, min(kb // 4, 148 // tiles, 8))
+    return max(1, min(kb // 16, 148 // tiles, 8))
 
 
 def layernorm(x, out=None, gamma=None, beta=None, shift=None, scale=None, eps=1e-6, mod_group=0):

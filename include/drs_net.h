@@ -67,6 +67,14 @@ int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C, const flo
 int drs_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                   void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale, void* stream);
 
+/* Same on the 5th-gen tensor cores (tcgen05.mma S = Q K^T and O += P V with TMEM
+ * accumulators, TMA-fed Q / K / V^T tiles, 128 queries per CTA).  V is given
+ * TRANSPOSED: vt[(h*d + j), b*vt_img + key] (row stride ldvt), as produced by a
+ * swapped-operand GEMM; vt_img >= Lk, multiple of 8.  d % 8 == 0, d <= 192. */
+int drs_attention_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* vt, int64_t ldvt,
+                     int vt_img, void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale,
+                     void* stream);
+
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);
 int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out_bf16, void* stream);

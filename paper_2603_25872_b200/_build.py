@@ -29,6 +29,7 @@ SOURCES = {                      # source -> extra flags
     "misc.cu": EXACT,
     "gemm_tc.cu": [],
     "net_ops.cu": [],
+    "attn_tc.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

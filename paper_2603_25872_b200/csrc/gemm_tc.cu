@@ -311,19 +311,30 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem_base);
 }
 
-// Deterministic split-K reduction + epilogue: one thread per (row, 32-col chunk).
+// Deterministic split-K reduction + epilogue.  A warp owns one row and 32
+// consecutive 32-column chunks: each lane sums its chunk's partials (fixed
+// split order) with float4 loads, then runs the common epilogue.
 __global__ void gemm_reduce_kernel(int M, int N, int split, EpiParams ep) {
   const int chunks = (N + 31) / 32;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)M * chunks) return;
-  const int row = (int)(idx / chunks), n0 = (int)(idx % chunks) * 32;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;          // host: M * chunks < 2^31
+  if (idx >= M * chunks) return;
+  const int row = idx / chunks, n0 = (idx - row * chunks) * 32;
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  const bool full = n0 + 32 <= N && (N % 4) == 0;
   for (int s = 0; s < split; ++s) {
     const float* src = ep.partial + ((int64_t)s * M + row) * N + n0;
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += src[j];
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(src) + q);
+        v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += src[j];
+    }
   }
   epilogue32(ep, M, N, row, n0, v);
 }

@@ -309,28 +309,31 @@ __global__ void silu_cast_kernel(const float* __restrict__ x, int64_t n, __nv_bf
 __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x1, int C1, const __nv_bfloat16* __restrict__ x2,
                               int C2, int N, int H, int W, int ks, int stride, int pad, int up, int Ho, int Wo,
                               __nv_bfloat16* __restrict__ out) {
-  const int C = C1 + C2, C8 = C / 8;
-  const int64_t total = (int64_t)N * Ho * Wo * ks * ks * C8;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 32-bit index math (host guarantees total < 2^31): one 16-byte chunk per thread
+  const int C8 = (C1 + C2) >> 3;
+  const int taps = ks * ks;
+  const int total = N * Ho * Wo * taps * C8;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= total) return;
-  const int c8 = (int)(i % C8);
-  int64_t r = i / C8;
-  const int tap = (int)(r % (ks * ks));
-  r /= (ks * ks);
-  const int ox = (int)(r % Wo);
-  const int oy = (int)((r / Wo) % Ho);
-  const int n = (int)(r / ((int64_t)Wo * Ho));
-  const int ky = tap / ks, kx = tap % ks;
+  const int c8 = i % C8;
+  int r = i / C8;
+  const int tap = r % taps;
+  r /= taps;
+  const int ox = r % Wo;
+  r /= Wo;
+  const int oy = r % Ho;
+  const int n = r / Ho;
+  const int ky = tap / ks, kx = tap - ky * ks;
   const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;   // in upsampled coordinates
   uint4 v = make_uint4(0, 0, 0, 0);
   if (iy >= 0 && ix >= 0 && iy < H * up && ix < W * up) {
     const int sy = iy / up, sx = ix / up;
-    const int64_t pix = ((int64_t)n * H + sy) * W + sx;
+    const int pix = (n * H + sy) * W + sx;
     const int c = c8 * 8;
-    v = c < C1 ? *reinterpret_cast<const uint4*>(x1 + pix * C1 + c)
-               : *reinterpret_cast<const uint4*>(x2 + pix * C2 + (c - C1));
+    v = c < C1 ? __ldg(reinterpret_cast<const uint4*>(x1 + (int64_t)pix * C1 + c))
+               : __ldg(reinterpret_cast<const uint4*>(x2 + (int64_t)pix * C2 + (c - C1)));
   }
-  *reinterpret_cast<uint4*>(out + i * 8) = v;
+  reinterpret_cast<uint4*>(out)[i] = v;
 }
 
 // GroupNorm over NHWC (bf16 or fp32 in) with affine and optional SiLU -> bf16.
@@ -405,20 +408,19 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
     const int g0 = c / cg, g1 = (c + 1) / cg;
     const float a0 = sstat[2 * g0 + 1] * gamma[c], a1 = sstat[2 * g1 + 1] * gamma[c + 1];
     const float b0 = beta[c] - sstat[2 * g0] * a0, b1 = beta[c + 1] - sstat[2 * g1] * a1;
-    for (int pp = 0; pp < kGnPix; ++pp) {
+    float2 v[kGnPix];
+#pragma unroll
+    for (int pp = 0; pp < kGnPix; ++pp) {            // all loads in flight first
       const int64_t off = (pix0 + pp) * C + c;
-      float v0, v1;
-      if (x_f32) {
-        const float2 f = *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off);
-        v0 = f.x; v1 = f.y;
-      } else {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off));
-        v0 = f.x; v1 = f.y;
-      }
-      v0 = v0 * a0 + b0;
-      v1 = v1 * a1 + b1;
+      v[pp] = x_f32 ? *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off)
+                    : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(
+                          static_cast<const __nv_bfloat16*>(x) + off));
+    }
+#pragma unroll
+    for (int pp = 0; pp < kGnPix; ++pp) {
+      float v0 = v[pp].x * a0 + b0, v1 = v[pp].y * a1 + b1;
       if (silu) { v0 = v0 / (1.f + __expf(-v0)); v1 = v1 / (1.f + __expf(-v1)); }
-      *reinterpret_cast<__nv_bfloat162*>(out + off) = __floats2bfloat162_rn(v0, v1);
+      *reinterpret_cast<__nv_bfloat162*>(out + (pix0 + pp) * C + c) = __floats2bfloat162_rn(v0, v1);
     }
   }
 }
@@ -535,6 +537,7 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
   if ((C1 % 8) || (C2 % 8) || (C2 && !x2) || ks < 1 || stride < 1 || up < 1) return DRS_ERR_VALUE;
   const int Ho = (H * up + 2 * pad - ks) / stride + 1, Wo = (W * up + 2 * pad - ks) / stride + 1;
   const int64_t total = (int64_t)N * Ho * Wo * ks * ks * ((C1 + C2) / 8);
+  if (total >= (1ll << 31)) return DRS_ERR_VALUE;
   im2col_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       static_cast<const __nv_bfloat16*>(x1), C1, static_cast<const __nv_bfloat16*>(x2), C2, N, H, W, ks, stride, pad,
       up, Ho, Wo, static_cast<__nv_bfloat16*>(out));

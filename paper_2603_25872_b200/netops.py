@@ -127,6 +127,18 @@ def attention(q, k, v, out, B, H, Lq, Lk, d, scale=None):
     return out
 
 
+def attention_tc(q, k, vt, out, B, H, Lq, Lk, d, scale=None, vt_img=None):
+    """tcgen05 attention; vt = V^T (H*d, >= B*vt_img) view, image b's keys at
+    columns b*vt_img.. (vt_img defaults to Lk and must be a multiple of 8)."""
+    scale = d ** -0.5 if scale is None else scale
+    vt_img = Lk if vt_img is None else vt_img
+    st = _lib.lib().drs_attention_tc(q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), vt.data_ptr(),
+                                     vt.stride(0), vt_img, out.data_ptr(), out.stride(0), B, H, Lq, Lk, d,
+                                     float(scale), _lib.stream_ptr())
+    _lib.check(st, "drs_attention_tc")
+    return out
+
+
 def timestep_embedding(t, dim, out, max_period=10000.0):
     _lib.check(_lib.lib().drs_timestep_embedding(t.data_ptr(), t.numel(), dim, float(max_period), out.data_ptr(),
                                                  _lib.stream_ptr()), "drs_timestep_embedding")

@@ -78,6 +78,7 @@ class UNet:
         self.cfg_scale = cfg_scale
         self.max_batch = max_batch                   # images per forward (each is a CFG pair)
         self.latent_numel = cfg.in_ch * cfg.size * cfg.size
+        self.ctx_pad = (cfg.ctx_len + 7) // 8 * 8
         I = _Init(self.device, seed)
         c0, T = cfg.channels[0], cfg.temb_dim
         self.p = p = {}
@@ -148,12 +149,22 @@ class UNet:
         for _ in range(depth):
             wk = I.mat(c, cfg.ctx_dim)
             wv = I.mat(c, cfg.ctx_dim)
-            if self.device.type == "cuda":                                     # fixed context: K/V once
-                kv = ops.linear(self.ctx, torch.cat([wk, wv], 0).contiguous())   # (2*ctx_len, 2c)
-            else:
-                kv = None                                                      # CPU copy: reference use only
+            k_ctx = vt_ctx = None
+            if self.device.type == "cuda":
+                # fixed context: K (rows) and V^T (columns) of every CFG image, once.
+                # image n uses context n % 2; V^T blocks are 8-aligned (TMA)
+                n_img = 2 * self.max_batch
+                ctx_all = self.ctx.view(2, cfg.ctx_len, cfg.ctx_dim).repeat(self.max_batch, 1, 1)
+                ctx_all = ctx_all.reshape(n_img * cfg.ctx_len, cfg.ctx_dim).contiguous()
+                k_ctx = ops.linear(ctx_all, wk)                                    # (n_img*77, c)
+                vt = ops.linear(wv, ctx_all)                                       # (c, n_img*77)
+                vt_ctx = torch.zeros(c, n_img * self.ctx_pad, dtype=torch.bfloat16, device=self.device)
+                for n in range(n_img):
+                    vt_ctx[:, n * self.ctx_pad:n * self.ctx_pad + cfg.ctx_len] = \
+                        vt[:, n * cfg.ctx_len:(n + 1) * cfg.ctx_len]
             layers.append(dict(ln1=I.gn(c), qkv=I.mat(3 * c, c), o1=(I.mat(c, c), I.vec(c)), ln2=I.gn(c),
-                               q2=I.mat(c, c), wk=wk, wv=wv, kv=kv, o2=(I.mat(c, c), I.vec(c)), ln3=I.gn(c),
+                               q2=I.mat(c, c), wk=wk, wv=wv, k_ctx=k_ctx, vt_ctx=vt_ctx,
+                               o2=(I.mat(c, c), I.vec(c)), ln3=I.gn(c),
                                ff1=(I.mat(8 * c, c), I.vec(8 * c)), ff2=(I.mat(c, 4 * c), I.vec(c))))
         return dict(c=c, gn=I.gn(c), pin=(I.mat(c, c), I.vec(c)), layers=layers, pout=(I.mat(c, c), I.vec(c)))
 
@@ -171,10 +182,10 @@ class UNet:
             self.flops += 2.0 * x.shape[0] * w.shape[0] * w.shape[1]
         return ops.linear(x, w, **kw)
 
-    def _attn(self, q, k, v, out, B, H, Lq, Lk, d):
+    def _attn(self, q, k, vt, out, B, H, Lq, Lk, d, vt_img):
         if self._count:
             self.flops += 4.0 * B * H * Lq * Lk * d
-        return ops.attention(q, k, v, out, B, H, Lq, Lk, d)
+        return ops.attention_tc(q, k, vt, out, B, H, Lq, Lk, d, vt_img=vt_img)
 
     def _conv3(self, x1, c1, x2, c2, N, H, W, wb, stride=1, up=1, **kw):
         Ho = (H * up + 2 - 3) // stride + 1
@@ -219,24 +230,21 @@ class UNet:
         s = self.buf(f"txs{c}_{HW}", (M, c), torch.float32)                   # fp32 residual stream
         self._lin(hn, t["pin"][0], bias=t["pin"][1], out=s)
         n1 = self.buf(f"txn{c}_{HW}", (M, c))
-        qkv = self.buf(f"qkv{c}_{HW}", (M, 3 * c))
+        qk = self.buf(f"qk{c}_{HW}", (M, 2 * c))
+        vt = self.buf(f"vt{c}_{HW}", (c, M))
         att = self.buf(f"att{c}_{HW}", (M, c))
         ffb = self.buf(f"ff{c}_{HW}", (M, 4 * c))
         for L in t["layers"]:
             ops.layernorm(s, out=n1, gamma=L["ln1"][0], beta=L["ln1"][1], eps=1e-5)
-            self._lin(n1, L["qkv"], out=qkv)
-            self._attn(qkv[:, :c], qkv[:, c:2 * c], qkv[:, 2 * c:], att, N, heads, HW, HW, d)
+            self._lin(n1, L["qkv"][:2 * c], out=qk)                       # Q | K
+            self._lin(L["qkv"][2 * c:], n1, out=vt)                       # V^T = Wv n1^T (swapped GEMM)
+            self._attn(qk[:, :c], qk[:, c:], vt, att, N, heads, HW, HW, d, HW)
             self._lin(att, L["o1"][0], bias=L["o1"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln2"][0], beta=L["ln2"][1], eps=1e-5)
-            q = qkv[:, :c]
+            q = qk[:, :c]
             self._lin(n1, L["q2"], out=q)
-            kv = L["kv"]
-            # image n uses context pair member n % 2 (uncond / cond)
-            for n in range(N):
-                j = n % 2
-                self._attn(q[n * HW:(n + 1) * HW], kv[j * cfg.ctx_len:(j + 1) * cfg.ctx_len, :c],
-                           kv[j * cfg.ctx_len:(j + 1) * cfg.ctx_len, c:], att[n * HW:(n + 1) * HW], 1, heads, HW,
-                           cfg.ctx_len, d)
+            # every image n attends to context n % 2 (uncond / cond): one launch
+            self._attn(q, L["k_ctx"], L["vt_ctx"], att, N, heads, HW, cfg.ctx_len, d, self.ctx_pad)
             self._lin(att, L["o2"][0], bias=L["o2"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln3"][0], beta=L["ln3"][1], eps=1e-5)
             self._lin(n1, L["ff1"][0], bias=L["ff1"][1], act="geglu", out=ffb)

@@ -104,3 +104,27 @@ def test_sd15_unet_vs_torch_fp32(cuda, size, g):
     rel = ((out.reshape(4, size, size) - ref).norm() / ref.norm()).item()
     assert torch.isfinite(out).all() and rel < 3e-2, rel
     assert net.flops > 0
+
+
+@pytest.mark.parametrize("B,H,Lq,Lk,d", [(1, 16, 256, 256, 72), (2, 8, 1024, 77, 40), (1, 5, 300, 300, 64),
+                                         (2, 8, 4096, 4096, 40), (1, 8, 128, 200, 160), (1, 2, 70, 33, 80),
+                                         (2, 10, 1024, 1024, 64)])
+def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d):
+    """tcgen05 attention (V given transposed) vs torch fp32."""
+    from paper_2603_25872_b200.netops import attention_tc
+    g = torch.Generator(device=cuda).manual_seed(Lq + d + 1)
+    q = torch.randn(B * Lq, 3 * H * d, device=cuda, generator=g).bfloat16()
+    k = torch.randn(B * Lk, 2 * H * d, device=cuda, generator=g).bfloat16()
+    v = torch.randn(B * Lk, H * d, device=cuda, generator=g).bfloat16()
+    vimg = (Lk + 7) // 8 * 8                          # TMA: 16-byte aligned per-image key blocks
+    vt = torch.zeros(H * d, B * vimg, device=cuda, dtype=torch.bfloat16)
+    for b in range(B):
+        vt[:, b * vimg:b * vimg + Lk] = v[b * Lk:(b + 1) * Lk].t()
+    out = torch.zeros(B * Lq, H * d, device=cuda, dtype=torch.bfloat16)
+    attention_tc(q[:, :H * d], k[:, :H * d], vt, out, B, H, Lq, Lk, d, vt_img=vimg)
+    Q = q[:, :H * d].float().reshape(B, Lq, H, d).transpose(1, 2)
+    K = k[:, :H * d].float().reshape(B, Lk, H, d).transpose(1, 2)
+    V = v.float().reshape(B, Lk, H, d).transpose(1, 2)
+    ref = (torch.softmax(Q @ K.transpose(-1, -2) / math.sqrt(d), -1) @ V).transpose(1, 2).reshape(B * Lq, H * d)
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel

@@ -127,6 +127,9 @@ double drs_host_exp(double x);
 int drs_host_seedseq(const drs_key* key, uint64_t seed, uint32_t* out, int n_words32);
 
 int drs_version(void);
+/* 1: launch every kernel with programmatic dependent launch so its prologue
+ * overlaps the predecessor's tail; 0 (default): plain stream ordering. */
+int drs_set_pdl(int on);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,10 @@ typedef struct drs_gemm_args {
   const float* rowbias; int rb_group; int64_t rb_ld;
   int bn, split;
   float* workspace;
+  /* implicit 3x3 conv (stride 1, pad 1): conv_C > 0 makes A the NHWC bf16
+   * input [conv_N, conv_H, conv_W, conv_C] (M = N*H*W, K = 9*C, weights
+   * (Cout, ky, kx, C)); C % 64 == 0, W a power of two <= 128. */
+  int conv_N, conv_H, conv_W, conv_C;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
 

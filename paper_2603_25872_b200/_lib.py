@@ -73,10 +73,11 @@ class DrsGemmArgs(ctypes.Structure):       # include/drs_net.h drs_gemm_args
         ("rowbias", ctypes.c_void_p), ("rb_group", ctypes.c_int), ("rb_ld", ctypes.c_int64),
         ("bn", ctypes.c_int), ("split", ctypes.c_int),
         ("workspace", ctypes.c_void_p),
+        ("conv_N", ctypes.c_int), ("conv_H", ctypes.c_int), ("conv_W", ctypes.c_int), ("conv_C", ctypes.c_int),
     ]
 
 
-assert ctypes.sizeof(DrsGemmArgs) == 168
+assert ctypes.sizeof(DrsGemmArgs) == 184
 assert ctypes.sizeof(DrsKey) == 48
 assert ctypes.sizeof(DrsOp) == 112
 
@@ -99,6 +100,7 @@ _SIGS = {
     "drs_host_seedseq": (ctypes.c_int, [ctypes.POINTER(DrsKey), ctypes.c_uint64,
                                         ctypes.POINTER(ctypes.c_uint32), ctypes.c_int]),
     "drs_version": (ctypes.c_int, []),
+    "drs_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     # include/drs_net.h
     "drs_gemm_bf16": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include "drs_net.h"
+#include "pdl.cuh"
 #include "tc_common.cuh"
 
 namespace drs {
@@ -126,6 +127,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  pdl_wait();       // everything above is data-independent setup (PDL overlap)
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;         // S0 at col 0, S1 at col 128, O at col 256
   if (threadIdx.x == 0) ATTN_TRACE(0, 1);
   uint8_t* sQ = smem + S::kQ;
@@ -347,7 +350,7 @@ static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
     attr = true;
   }
   dim3 grid((Lq + kAQ - 1) / kAQ, H, B);
-  kern<<<grid, kAttnTcThreads, S::kBytes, st>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(o), ldo, Lq, Lk, d, vt_img,
+  launch_pdl(kern, dim3(grid), dim3(kAttnTcThreads), S::kBytes, st, tq, tk, tv, static_cast<__nv_bfloat16*>(o), ldo, Lq, Lk, d, vt_img,
                                                 sl2);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

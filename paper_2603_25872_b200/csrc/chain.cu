@@ -14,6 +14,7 @@
 // reference's own scalar expressions (paper_2603_25872_b200/transitions.py).
 #include <cuda_runtime.h>
 #include "drs.h"
+#include "pdl.cuh"
 
 namespace drs {
 
@@ -28,6 +29,8 @@ __device__ __forceinline__ double load_eps(const drs_op& op, int64_t j) {
 
 __global__ void __launch_bounds__(kChainThreads)
 skip_chain_kernel(const drs_op* __restrict__ ops, int n_ops, int64_t D) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ drs_op s_ops[kMaxOps];
   {
     const uint64_t* src = reinterpret_cast<const uint64_t*>(ops);
@@ -97,6 +100,6 @@ extern "C" int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* str
   if (!ops) return DRS_ERR_VALUE;
   int64_t blocks = (D + drs::kChainThreads - 1) / drs::kChainThreads;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  drs::skip_chain_kernel<<<(unsigned)blocks, drs::kChainThreads, 0, (cudaStream_t)stream>>>(ops, n_ops, D);
+  drs::launch_pdl(drs::skip_chain_kernel, dim3((unsigned)blocks), dim3(drs::kChainThreads), 0, (cudaStream_t)stream, ops, n_ops, D);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include "drs_net.h"
+#include "pdl.cuh"
 #include "tc_common.cuh"
 
 namespace drs {
@@ -167,6 +168,26 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int
   }
 }
 
+// Implicit-GEMM 3x3 convolution (stride 1, pad 1) over an NHWC bf16 input:
+// A[(n,y,x), (ky,kx,c)] is never materialised -- the k-block (tap, 64-channel
+// block) of a 128-pixel tile is ONE 4-D TMA box {64 ch, W, rows, images} of
+// the input at (c0, x0 + kx - 1, y0 + ky - 1, n0); TMA zero-fills the
+// out-of-image taps, which is exactly the zero padding.
+struct ConvGeom {
+  int on;          // 0: plain GEMM (2-D A map)
+  int cblocks;     // Cin / 64
+  int H, W;        // image size (W <= 128, W * rows * imgs == 128 pixels per tile)
+};
+
+__device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 template <int BN, int kStages>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
@@ -179,7 +200,7 @@ struct GemmSmem {
 template <int BN, int kStages>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    int M, int N, int K, int split, EpiParams ep) {
+                    int M, int N, int K, int split, EpiParams ep, ConvGeom cv) {
   using S = GemmSmem<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -208,6 +229,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  pdl_wait();       // everything above is data-independent setup (PDL overlap)
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -226,7 +249,15 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
           tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
-          tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
+          if (cv.on) {
+            const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
+            const int ky = tap / 3, kx = tap - ky * 3;
+            const int m0 = mt * kBM, hw = cv.H * cv.W;
+            const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+            tma_load_4d(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+          } else {
+            tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
+          }
           tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -315,6 +346,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
 // consecutive 32-column chunks: each lane sums its chunk's partials (fixed
 // split order) with float4 loads, then runs the common epilogue.
 __global__ void gemm_reduce_kernel(int M, int N, int split, EpiParams ep) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = (N + 31) / 32;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;          // host: M * chunks < 2^31
   if (idx >= M * chunks) return;
@@ -369,6 +402,21 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// NHWC input as {C, W, H, N}; box {64 ch, W, rows, imgs} with W * rows * imgs == 128
+static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const int rows = W >= 128 ? 1 : (128 / W <= H ? 128 / W : H);
+  const int imgs = 128 / (W * rows);
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -381,7 +429,7 @@ static int num_sms() {
 
 template <int BN, int kStages>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
-                       const EpiParams& ep, cudaStream_t st) {
+                       const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
   auto kern = gemm_bf16_tc_kernel<BN, kStages>;
   static bool attr = false;
@@ -392,7 +440,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kGemmThreads, S::kBytes, st>>>(ta, tb, M, N, K, split, ep);
+  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, M, N, K, split, ep, cv);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
@@ -404,7 +452,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   const int M = g->M, N = g->N, K = g->K;
   if (M <= 0 || N <= 0 || K <= 0) return (M == 0 || N == 0) ? DRS_OK : DRS_ERR_VALUE;
   if (!g->A || !g->B || !g->C) return DRS_ERR_VALUE;
-  if ((K % 8) || (g->lda % 8) || (g->ldb % 8)) return DRS_ERR_VALUE;     // TMA: 16-byte row strides
+  if ((K % 8) || (!g->conv_C && (g->lda % 8)) || (g->ldb % 8)) return DRS_ERR_VALUE;   // TMA: 16-byte strides
   if ((reinterpret_cast<uintptr_t>(g->A) & 15) || (reinterpret_cast<uintptr_t>(g->B) & 15)) return DRS_ERR_VALUE;
   if (g->act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
   if (g->rowbias && g->rb_group <= 0) return DRS_ERR_VALUE;
@@ -413,19 +461,31 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   const int split = g->split < 1 ? 1 : g->split;
   if (split > 1 && !g->workspace) return DRS_ERR_VALUE;
   CUtensorMap ta, tb;
-  if (!make_tmap(&ta, g->A, M, K, g->lda, kBM) || !make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
+  ConvGeom cv{0, 0, 0, 0};
+  if (g->conv_C > 0) {      // implicit 3x3 conv: A = NHWC input, M = N*H*W, K = 9*C
+    const int C = g->conv_C, H = g->conv_H, W = g->conv_W, Nimg = g->conv_N;
+    if (C % 64 || W > 128 || (W & (W - 1)) || (int64_t)Nimg * H * W != M || K != 9 * C) return DRS_ERR_VALUE;
+    const int rows = W >= 128 ? 1 : (128 / W <= H ? 128 / W : H);
+    if (W * rows * (128 / (W * rows)) != 128 || H % rows || (128 / (W * rows) > 1 && (rows != H || Nimg % (128 / (W * H)))))
+      return DRS_ERR_VALUE;
+    if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C)) return DRS_ERR_CUDA;
+    cv = ConvGeom{1, C / 64, H, W};
+  } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
+    return DRS_ERR_CUDA;
+  }
+  if (!make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, g->workspace};
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, st);
-  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, M, N, K, split, ep, st);
-  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, M, N, K, split, ep, st);
-  else if (bn == 192) rc = launch_gemm<192, 5>(ta, tb, M, N, K, split, ep, st);
-  else rc = launch_gemm<256, 4>(ta, tb, M, N, K, split, ep, st);
+  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, cv, st);
+  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, M, N, K, split, ep, cv, st);
+  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, M, N, K, split, ep, cv, st);
+  else if (bn == 192) rc = launch_gemm<192, 5>(ta, tb, M, N, K, split, ep, cv, st);
+  else rc = launch_gemm<256, 4>(ta, tb, M, N, K, split, ep, cv, st);
   if (rc != DRS_OK || split == 1) return rc;
   const int64_t threads = (int64_t)M * ((N + 31) / 32);
-  gemm_reduce_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(M, N, split, ep);
+  launch_pdl(gemm_reduce_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, M, N, split, ep);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include "drs.h"
+#include "pdl.cuh"
 
 namespace drs {
 
@@ -31,6 +32,8 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
               const double* __restrict__ alpha_bar, int T, const double* __restrict__ means,
               const double* __restrict__ log_w, const double* __restrict__ var, int n_comp,
               double* const* __restrict__ outs, int* __restrict__ err) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[kGmMaxComp][32];
   __shared__ double s_r[kGmMaxComp];
   const int row = blockIdx.x;
@@ -160,7 +163,7 @@ extern "C" int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows
   if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmMaxComp || T < 0) return DRS_ERR_VALUE;
   if (n_rows == 0 || D == 0) return DRS_OK;
   if (!xs || !ts || !alpha_bar || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
-  drs::gm_eps_kernel<<<n_rows, drs::kGmThreads, 0, (cudaStream_t)stream>>>(
+  drs::launch_pdl(drs::gm_eps_kernel, dim3(n_rows), dim3(drs::kGmThreads), 0, (cudaStream_t)stream, 
       xs, ts, D, alpha_bar, T, means, log_w, var, n_comp, out, err);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -1,6 +1,7 @@
 // Small device utilities + host-side test hooks of libdrs.so.
 #include <cuda_runtime.h>
 #include "drs.h"
+#include "pdl.cuh"
 #include "bitgen.cuh"
 #include "glibc_math.cuh"
 
@@ -8,6 +9,8 @@ namespace drs {
 
 __global__ void copy_rows_kernel(const double* const* __restrict__ src, double* const* __restrict__ dst,
                                  int64_t D) {
+  pdl_wait();
+  pdl_trigger();
   const double* s = src[blockIdx.y];
   double* d = dst[blockIdx.y];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < D;
@@ -18,6 +21,8 @@ __global__ void copy_rows_kernel(const double* const* __restrict__ src, double* 
 // Busy-wait on the global nanosecond timer: the GPU stand-in for the
 // reference Latency wrapper's time.sleep (denoiser.py:258-263).
 __global__ void spin_kernel(uint64_t ns) {
+  pdl_wait();
+  pdl_trigger();
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
@@ -38,14 +43,14 @@ extern "C" int drs_copy_rows(const double* const* src, double* const* out, int n
   int64_t bx = (D + 255) / 256;
   if (bx > 1024) bx = 1024;
   dim3 grid((unsigned)bx, (unsigned)n_rows);
-  drs::copy_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, out, D);
+  drs::launch_pdl(drs::copy_rows_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, src, out, D);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
 extern "C" int drs_spin(double us, int n_ctas, void* stream) {
   if (!(us >= 0.0) || n_ctas < 0) return DRS_ERR_VALUE;
   if (n_ctas == 0 || us == 0.0) return DRS_OK;
-  drs::spin_kernel<<<n_ctas, 32, 0, (cudaStream_t)stream>>>((uint64_t)(us * 1000.0));
+  drs::launch_pdl(drs::spin_kernel, dim3(n_ctas), dim3(32), 0, (cudaStream_t)stream, (uint64_t)(us * 1000.0));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
@@ -63,3 +68,8 @@ extern "C" int drs_host_seedseq(const drs_key* key, uint64_t seed, uint32_t* out
 }
 
 extern "C" int drs_version(void) { return 1; }
+
+extern "C" int drs_set_pdl(int on) {
+  drs::pdl_enabled() = on ? 1 : 0;
+  return DRS_OK;
+}

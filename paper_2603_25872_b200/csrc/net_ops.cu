@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdint.h>
 #include "drs_net.h"
+#include "pdl.cuh"
 
 namespace drs {
 
@@ -20,6 +21,8 @@ __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_
                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                  const float* __restrict__ shift, const float* __restrict__ scale, int mod_group,
                                  int64_t mod_ld, float eps, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -112,6 +115,8 @@ __global__ void __launch_bounds__(kAttnThreads)
 attention_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq, const __nv_bfloat16* __restrict__ k,
                  int64_t ldk, const __nv_bfloat16* __restrict__ v, int64_t ldv, __nv_bfloat16* __restrict__ o,
                  int64_t ldo, int Lq, int Lk, int d, float scale_log2) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int LD = DP + 8;            // smem row stride (elements): 16 B aligned, staggers banks
   __shared__ __align__(16) __nv_bfloat16 sQ[kAttnBQ * LD];
   __shared__ __align__(16) __nv_bfloat16 sK[BK * LD];
@@ -247,6 +252,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq, const __nv_bf
 // emb[i] = [cos(t f_j), sin(t f_j)], f_j = exp(-ln(max_period) j / half)  (DiT TimestepEmbedder)
 __global__ void timestep_embedding_kernel(const float* __restrict__ t, int n, int dim, float max_period,
                                           __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int half = dim / 2;
   if (i >= n * half) return;
@@ -260,6 +267,8 @@ __global__ void timestep_embedding_kernel(const float* __restrict__ t, int n, in
 // latent x (C, H, W) fp64/fp32 -> tokens (H/p * W/p, C*p*p) bf16, feature order (c, py, px)
 __global__ void patchify_kernel(const void* __restrict__ x, int x_f64, int C, int H, int W, int p,
                                 __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int gw = W / p, feat = C * p * p;
   if (i >= (H / p) * gw * feat) return;
@@ -274,6 +283,8 @@ __global__ void patchify_kernel(const void* __restrict__ x, int x_f64, int C, in
 // tokens (H/p * W/p, p*p*Cout) fp32, feature order (py, px, c) -> eps (Ckeep, H, W) fp32
 __global__ void unpatchify_kernel(const float* __restrict__ tok, int Cout, int Ckeep, int H, int W, int p,
                                   float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= Ckeep * H * W) return;
   const int c = i / (H * W), hh = (i / W) % H, ww = i % W;
@@ -284,6 +295,8 @@ __global__ void unpatchify_kernel(const float* __restrict__ tok, int Cout, int C
 }
 
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i + 3 < n) {
     const float4 v = *reinterpret_cast<const float4*>(x + i);
@@ -297,6 +310,8 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, int64_t n, __n
 }
 
 __global__ void silu_cast_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { const float a = x[i]; out[i] = __float2bfloat16(a / (1.f + __expf(-a))); }
 }
@@ -309,6 +324,8 @@ __global__ void silu_cast_kernel(const float* __restrict__ x, int64_t n, __nv_bf
 __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x1, int C1, const __nv_bfloat16* __restrict__ x2,
                               int C2, int N, int H, int W, int ks, int stride, int pad, int up, int Ho, int Wo,
                               __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   // 32-bit index math (host guarantees total < 2^31): one 16-byte chunk per thread
   const int C8 = (C1 + C2) >> 3;
   const int taps = ks * ks;
@@ -346,6 +363,8 @@ constexpr int kGnSplit = 16;
 
 __global__ void gn_stats_kernel(const void* __restrict__ x, int x_f32, int HW, int C, int G,
                                 float2* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   const int ng = blockIdx.x, sp = blockIdx.y;
   const int n = ng / G, g = ng % G, cg = C / G;
   const int p0 = (int)((int64_t)HW * sp / kGnSplit), p1 = (int)((int64_t)HW * (sp + 1) / kGnSplit);
@@ -387,6 +406,8 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
                                 const float2* __restrict__ part, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, float eps, int silu,
                                 __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sstat[];                  // [G][2] mean, rstd
   const int64_t pix0 = (int64_t)blockIdx.x * kGnPix;  // global pixel index (n*HW + p)
   const int n = (int)(pix0 / HW);
@@ -428,6 +449,8 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
 // latent (C, H, W) fp64/fp32 -> NHWC bf16 with Cpad channels (zeros beyond C)
 __global__ void latent_to_nhwc_kernel(const void* __restrict__ x, int x_f64, int C, int HW, int Cpad,
                                       __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= HW * Cpad) return;
   const int p = i / Cpad, c = i % Cpad;
@@ -441,6 +464,8 @@ __global__ void latent_to_nhwc_kernel(const void* __restrict__ x, int x_f64, int
 // columns); eps (C, H, W) = u + g (c - u).  g == 1 or ld == 0: single image.
 __global__ void cfg_combine_kernel(const float* __restrict__ y, int64_t ld, int HW, int C, float g, int pair,
                                    float* __restrict__ eps) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C * HW) return;
   const int c = i / HW, p = i % HW;
@@ -464,7 +489,7 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
   cudaStream_t st = (cudaStream_t)stream;
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
   const int v4 = (C / 4 + 31) / 32;
-#define DRS_LN(K) layernorm_kernel<K><<<grid, warps * 32, 0, st>>>(x, ldx, x_f32, M, C, gamma, beta, shift, scale, \
+#define DRS_LN(K) launch_pdl(layernorm_kernel<K>, dim3(grid), dim3(warps * 32), 0, st, x, ldx, x_f32, M, C, gamma, beta, shift, scale, \
                                                                   mod_group, mod_ld, eps, o, ldo)
   if (v4 <= 4) DRS_LN(4);
   else if (v4 <= 8) DRS_LN(8);
@@ -488,14 +513,14 @@ extern "C" int drs_attention(const void* q, int64_t ldq, const void* k, int64_t 
   auto V = static_cast<const __nv_bfloat16*>(v);
   auto O = static_cast<__nv_bfloat16*>(o);
   switch (DP) {
-    case 16: attention_kernel<16><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 32: attention_kernel<32><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 48: attention_kernel<48><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 64: attention_kernel<64><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 80: attention_kernel<80><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 96: attention_kernel<96><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 128: attention_kernel<128><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
-    case 160: attention_kernel<160><<<grid, kAttnThreads, 0, st>>>(Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 16: launch_pdl(attention_kernel<16>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 32: launch_pdl(attention_kernel<32>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 48: launch_pdl(attention_kernel<48>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 64: launch_pdl(attention_kernel<64>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 80: launch_pdl(attention_kernel<80>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 96: launch_pdl(attention_kernel<96>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 128: launch_pdl(attention_kernel<128>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
+    case 160: launch_pdl(attention_kernel<160>, dim3(grid), dim3(kAttnThreads), 0, st, Q, ldq, K, ldk, V, ldv, O, ldo, Lq, Lk, d, sl2); break;
     default: return DRS_ERR_VALUE;
   }
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
@@ -504,7 +529,7 @@ extern "C" int drs_attention(const void* q, int64_t ldq, const void* k, int64_t 
 extern "C" int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out, void* stream) {
   if (n <= 0 || dim <= 0 || dim % 2) return DRS_ERR_VALUE;
   const int tot = n * dim / 2;
-  timestep_embedding_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(timestep_embedding_kernel, dim3((tot + 255) / 256), dim3(256), 0, (cudaStream_t)stream, 
       t, n, dim, max_period, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
@@ -512,7 +537,7 @@ extern "C" int drs_timestep_embedding(const float* t, int n, int dim, float max_
 extern "C" int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out, void* stream) {
   if (p <= 0 || H % p || W % p) return DRS_ERR_VALUE;
   const int tot = C * H * W;
-  patchify_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, x_f64, C, H, W, p,
+  launch_pdl(patchify_kernel, dim3((tot + 255) / 256), dim3(256), 0, (cudaStream_t)stream, x, x_f64, C, H, W, p,
                                                                        static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
@@ -520,14 +545,14 @@ extern "C" int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p
 extern "C" int drs_unpatchify(const float* tok, int Cout, int Ckeep, int H, int W, int p, float* out, void* stream) {
   if (p <= 0 || H % p || W % p || Ckeep > Cout) return DRS_ERR_VALUE;
   const int tot = Ckeep * H * W;
-  unpatchify_kernel<<<(tot + 255) / 256, 256, 0, (cudaStream_t)stream>>>(tok, Cout, Ckeep, H, W, p, out);
+  launch_pdl(unpatchify_kernel, dim3((tot + 255) / 256), dim3(256), 0, (cudaStream_t)stream, tok, Cout, Ckeep, H, W, p, out);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
 extern "C" int drs_silu_cast(const float* x, int64_t n, void* out, void* stream) {
   if (n < 0) return DRS_ERR_VALUE;
   if (n == 0) return DRS_OK;
-  silu_cast_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(silu_cast_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, 
       x, n, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
@@ -538,7 +563,7 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
   const int Ho = (H * up + 2 * pad - ks) / stride + 1, Wo = (W * up + 2 * pad - ks) / stride + 1;
   const int64_t total = (int64_t)N * Ho * Wo * ks * ks * ((C1 + C2) / 8);
   if (total >= (1ll << 31)) return DRS_ERR_VALUE;
-  im2col_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(im2col_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, 
       static_cast<const __nv_bfloat16*>(x1), C1, static_cast<const __nv_bfloat16*>(x2), C2, N, H, W, ks, stride, pad,
       up, Ho, Wo, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
@@ -550,23 +575,23 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
     return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
   float2* part = static_cast<float2*>(workspace);    // N*G*kGnSplit float2
-  gn_stats_kernel<<<dim3(N * G, kGnSplit), 256, 0, st>>>(x, x_f32, HW, C, G, part);
+  launch_pdl(gn_stats_kernel, dim3(dim3(N * G, kGnSplit)), dim3(256), 0, st, x, x_f32, HW, C, G, part);
   const int c2 = C / 2, thr = c2 >= 256 ? 256 : ((c2 + 31) / 32) * 32;
-  gn_apply_kernel<<<(unsigned)((int64_t)N * HW / kGnPix), thr, 2 * G * sizeof(float), st>>>(
+  launch_pdl(gn_apply_kernel, dim3((unsigned)((int64_t)N * HW / kGnPix)), dim3(thr), 2 * G * sizeof(float), st, 
       x, x_f32, HW, C, G, part, gamma, beta, eps, silu, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
 extern "C" int drs_latent_to_nhwc(const void* x, int x_f64, int C, int HW, int Cpad, void* out, void* stream) {
   if (Cpad < C) return DRS_ERR_VALUE;
-  latent_to_nhwc_kernel<<<(HW * Cpad + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(latent_to_nhwc_kernel, dim3((HW * Cpad + 255) / 256), dim3(256), 0, (cudaStream_t)stream, 
       x, x_f64, C, HW, Cpad, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
 extern "C" int drs_cfg_combine(const float* y, int64_t ld, int HW, int C, float g, int pair, float* eps,
                                void* stream) {
-  cfg_combine_kernel<<<(C * HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(y, ld, HW, C, g, pair, eps);
+  launch_pdl(cfg_combine_kernel, dim3((C * HW + 255) / 256), dim3(256), 0, (cudaStream_t)stream, y, ld, HW, C, g, pair, eps);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
@@ -574,7 +599,7 @@ extern "C" int drs_cast_f32_bf16(const float* x, int64_t n, void* out, void* str
   if (n < 0 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 7)) return DRS_ERR_VALUE;
   if (n == 0) return DRS_OK;
   const int64_t th = (n + 3) / 4;
-  cast_f32_bf16_kernel<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(cast_f32_bf16_kernel, dim3((unsigned)((th + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, 
       x, n, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

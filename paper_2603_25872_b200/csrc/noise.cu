@@ -26,6 +26,7 @@
 // FMA-variant log1p/exp ported in glibc_math.cuh.
 #include <cuda_runtime.h>
 #include "drs.h"
+#include "pdl.cuh"
 #include "bitgen.cuh"
 #include "glibc_math.cuh"
 
@@ -135,6 +136,8 @@ __device__ __forceinline__ void load_key(const drs_key* keys, const uint64_t* se
 __global__ void __launch_bounds__(kThreads)
 noise_pcg64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
                    int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t words[kWords];
   __shared__ double vals[kW];
   __shared__ uint8_t steps[kW];               // bit7 = accept, bits0..6 = words consumed
@@ -194,6 +197,8 @@ constexpr int kSfcWorkers = kThreads - 32;
 __global__ void __launch_bounds__(kThreads)
 noise_sfc64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict__ seeds,
                    int64_t n, double* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint64_t words[2][kSfcWords];
   __shared__ double vals[kSfcW];
   __shared__ uint8_t steps[kSfcW];
@@ -252,9 +257,9 @@ extern "C" int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const
   if (!keys || !out || !err) return DRS_ERR_VALUE;
   cudaStream_t s = (cudaStream_t)stream;
   if (gen == DRS_GEN_PCG64)
-    drs::noise_pcg64_kernel<<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+    drs::launch_pdl(drs::noise_pcg64_kernel, dim3(n_streams), dim3(drs::kThreads), 0, s, keys, seeds, n, out, ld, err);
   else if (gen == DRS_GEN_SFC64)
-    drs::noise_sfc64_kernel<<<n_streams, drs::kThreads, 0, s>>>(keys, seeds, n, out, ld, err);
+    drs::launch_pdl(drs::noise_sfc64_kernel, dim3(n_streams), dim3(drs::kThreads), 0, s, keys, seeds, n, out, ld, err);
   else
     return DRS_ERR_VALUE;
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;

@@ -1,0 +1,43 @@
+// Programmatic dependent launch (PDL) for every libdrs kernel.
+//
+// Kernels are launched with cudaLaunchAttributeProgrammaticStreamSerialization,
+// so a kernel's CTAs may start while its predecessor on the stream is still
+// draining.  Every kernel therefore calls pdl_wait() (griddepcontrol.wait)
+// before its first read of data a predecessor may produce -- after its
+// data-independent prologue (mbarrier init, TMEM allocation, tensor-map
+// prefetch) -- and pdl_trigger() (griddepcontrol.launch_dependents) once it is
+// resident, so the next kernel's launch latency and prologue overlap this
+// kernel's tail.  The chain is transitive: when pdl_wait() returns, every
+// earlier kernel on the stream has completed and its writes are visible.
+// Works inside CUDA-graph capture (programmatic edges).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace drs {
+
+// runtime switch (drs_set_pdl): 1 = launch with the PDL attribute, 0 = plain stream order
+inline int& pdl_enabled() {
+  static int on = 0;   // measured: +1.5% on the SD1.5 UNet, -16% on batch-1 DiT -> off by default
+  return on;
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace drs

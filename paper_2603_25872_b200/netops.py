@@ -31,19 +31,25 @@ def _ptr(t):
 
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
-           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0):
+           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
-    M, K = x.shape
+    if conv is not None:          # implicit 3x3 conv: x is NHWC (N*H*W, C), K = 9*C
+        cn, ch, cw, cc = conv
+        M, K = cn * ch * cw, 9 * cc
+    else:
+        M, K = x.shape
     N = w.shape[0]
-    assert w.shape[1] == K and x.stride(1) == 1 and w.stride(1) == 1
+    assert w.shape[1] == K and x.stride(-1) == 1 and w.stride(1) == 1
     n_out = N // 2 if act == "geglu" else N
     if out is None:
         out = torch.empty(M, n_out, dtype=out_dtype, device=x.device)
     g = _lib.DrsGemmArgs()
     g.A, g.lda, g.B, g.ldb, g.C, g.ldc = x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), out.data_ptr(), out.stride(0)
+    if conv is not None:
+        g.lda = K
     g.M, g.N, g.K = M, N, K
     g.act, g.out_f32, g.alpha = ACT[act], 1 if out.dtype == torch.float32 else 0, float(alpha)
     if bias is not None:
@@ -64,6 +70,8 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     if split == 0:
         split = pick_split(M, N, K, bn)
     g.bn, g.split = bn, split
+    if conv is not None:
+        g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
     if split > 1:
         g.workspace = _workspace(x.device, split * M * N).data_ptr()
     if TIMERS is not None:

@@ -188,6 +188,18 @@ class UNet:
         return ops.attention_tc(q, k, vt, out, B, H, Lq, Lk, d, vt_img=vt_img)
 
     def _conv3(self, x1, c1, x2, c2, N, H, W, wb, stride=1, up=1, **kw):
+        """3x3 conv, pad 1.  Stride-1 convs on one NHWC tensor run as implicit
+        GEMMs (A tiles are 4-D TMA boxes of the input; no im2col); a nearest-2x
+        upsample is materialised first (4x, vs 9x for im2col); the stride-2
+        downsamples go through im2col."""
+        if x2 is None and stride == 1 and c1 % 64 == 0:
+            if up == 2:
+                xu = self.buf(f"ups{c1}_{H}", (N * 4 * H * W, c1))
+                ops.im2col(x1, c1, None, 0, N, H, W, 1, 1, 0, 2, xu)
+                x1, H, W = xu, 2 * H, 2 * W
+            if self._count:
+                self.flops += 2.0 * N * H * W * wb[0].shape[0] * wb[0].shape[1]
+            return ops.linear(x1, wb[0], bias=wb[1], conv=(N, H, W, c1), **kw), H, W
         Ho = (H * up + 2 - 3) // stride + 1
         Wo = (W * up + 2 - 3) // stride + 1
         A = self.buf("im2col", (N * Ho * Wo, 9 * (c1 + c2)))

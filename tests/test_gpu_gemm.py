@@ -52,3 +52,21 @@ def test_gemm_epilogues(cuda, act, split):
     ref = _ref(x, w, b, act, r, 0.5)
     rel = ((y.float() - ref).norm() / ref.norm()).item()
     assert y.shape == (M, n_out) and rel <= 8e-3, (act, split, rel)
+
+
+@pytest.mark.parametrize("N,H,W,C,Co", [(2, 64, 64, 320, 320), (2, 32, 32, 640, 640), (2, 16, 16, 1280, 1280),
+                                        (2, 8, 8, 1280, 1280), (1, 128, 128, 64, 320), (4, 8, 8, 128, 64),
+                                        (2, 32, 32, 64, 4)])
+def test_implicit_conv3x3(cuda, N, H, W, C, Co):
+    """Implicit-GEMM 3x3 conv (4-D TMA boxes, zero-fill padding) vs torch conv2d (fp32)."""
+    import torch.nn.functional as F
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(H * C + Co)
+    x = torch.randn(N, H, W, C, device=cuda, generator=g).bfloat16()             # NHWC
+    w = (torch.randn(Co, 3, 3, C, device=cuda, generator=g) * 0.05).bfloat16()    # (Co, ky, kx, C)
+    b = torch.randn(Co, device=cuda, generator=g) * 0.1
+    y = linear(x.reshape(N * H * W, C), w.reshape(Co, 9 * C), bias=b, out_dtype=torch.float32, conv=(N, H, W, C))
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), b, padding=1)
+    ref = ref.permute(0, 2, 3, 1).reshape(N * H * W, Co)
+    rel = ((y - ref).norm() / ref.norm()).item()
+    assert rel < 5e-3, rel

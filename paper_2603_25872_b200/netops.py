@@ -102,6 +102,18 @@ def pick_bn(M, N, sms=148):
     return best
 
 
+def implicit_conv_ok(N, H, W, C):
+    """Geometry the implicit-GEMM conv supports (mirrors drs_gemm's checks):
+    128-pixel tiles of whole image rows (or whole images) of an NHWC input."""
+    if C % 64 or W > 128 or W & (W - 1):
+        return False
+    rows = 1 if W >= 128 else min(128 // W, H)
+    imgs = 128 // (W * rows)
+    if W * rows * imgs != 128 or H % rows:
+        return False
+    return imgs == 1 or (rows == H and N % imgs == 0)
+
+
 def pick_split(M, N, K, bn):
     """Deterministic split-K (fp32 partials + fixed-order reduce) when the tile
     grid leaves most SMs idle AND each split still has a long K loop."""

@@ -192,7 +192,7 @@ class UNet:
         GEMMs (A tiles are 4-D TMA boxes of the input; no im2col); a nearest-2x
         upsample is materialised first (4x, vs 9x for im2col); the stride-2
         downsamples go through im2col."""
-        if x2 is None and stride == 1 and c1 % 64 == 0:
+        if x2 is None and stride == 1 and ops.implicit_conv_ok(N, H * up, W * up, c1):
             if up == 2:
                 xu = self.buf(f"ups{c1}_{H}", (N * 4 * H * W, c1))
                 ops.im2col(x1, c1, None, 0, N, H, W, 1, 1, 0, 2, xu)

@@ -8,10 +8,13 @@
 //   warp 1      TMEM allocator + MMA issuer:  S_j = Q K_j^T   (M=128, N=128, K=DP)
 //               into one of two TMEM S buffers, then O += P_j V_j (M=128, N=DP,
 //               K=128) into the TMEM O accumulator
-//   warps 2..5  softmax: thread = query row = TMEM lane; tcgen05.ld the S row,
-//               online max / exp2 / sum, rescale the O row in TMEM only when the
-//               running max moved, write P (bf16) into shared memory in the UMMA
-//               SWIZZLE_128B K-major layout, then the final O / l epilogue.
+//   warps 2..9  softmax, two warps per TMEM lane quadrant: a query row (TMEM
+//               lane) is shared by two threads that each own 64 of the 128 key
+//               columns (and half of the O columns): tcgen05.ld their half of S,
+//               exchange the row max through shared memory, exp2 / partial sums,
+//               rescale their half of the O row only when the running max moved,
+//               write their half of P (bf16) in the UMMA SWIZZLE_128B K-major
+//               layout; the partial row sums are combined once, in the epilogue.
 // Operands: Q and K through 3-D tensor maps (elem, head, row) so head dims that
 // are not multiples of 64 are zero-filled by TMA up to DP; V is consumed as V^T
 // (channels x keys, keys contiguous -- produced directly by a swapped-operand
@@ -28,7 +31,7 @@ namespace drs {
 
 constexpr int kAQ = 128;       // queries per CTA
 constexpr int kAK = 128;       // keys per tile
-constexpr int kAttnTcThreads = 192;
+constexpr int kAttnTcThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 softmax (2 per TMEM quadrant)
 
 // Debug aid: when set (drs_attention_tc_debug), CTAs record per-role progress
 // markers into host-mapped memory the CPU can read while a launch is stuck.
@@ -57,7 +60,8 @@ struct AttnSmem {
   static constexpr int kK = kQ + kQBytes;
   static constexpr int kV = kK + kStages * kKBytes;
   static constexpr int kP = kV + kStages * kVBytes;
-  static constexpr int kBar = kP + kPBytes;
+  static constexpr int kRed = kP + kPBytes;                // [2 halves][128 rows] float row maxima / sums
+  static constexpr int kBar = kRed + 2 * kAQ * 4;
   // >= 116 KB so two CTAs never share an SM: each allocates all 512 TMEM columns
   static constexpr int kRaw = kBar + 16 * 8 + 16 + 1024;
   static constexpr int kBytes = kRaw < 116 * 1024 ? 116 * 1024 : kRaw;
@@ -101,7 +105,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* kv_full = bars + 1;            // kSt
   uint64_t* kv_empty = bars + 3;           // kSt
   uint64_t* s_full = bars + 5;             // 2 (per S buffer)
-  uint64_t* p_full = bars + 7;             // 1 (count 4: softmax warps)
+  uint64_t* p_full = bars + 7;             // 1 (count 8: softmax warps)
   uint64_t* o_done = bars + 8;             // 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
@@ -119,7 +123,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int s = 0; s < kSt; ++s) { tc::mbar_init(&kv_full[s], 1); tc::mbar_init(&kv_empty[s], 1); }
     tc::mbar_init(&s_full[0], 1);
     tc::mbar_init(&s_full[1], 1);
-    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_full, 8);
     tc::mbar_init(o_done, 1);
     tc::fence_barrier_init();
   }
@@ -197,31 +201,43 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (kSt == 1 && j + 1 < n_tiles) issue_s(j + 1);
     }
   } else {
-    // softmax warps: warp w owns TMEM lanes 32*(w&3) .. +31, i.e. query rows
+    // softmax warps: warp w owns TMEM lanes 32*(w&3) .. +31 (query rows) and
+    // the half (w-2)>>2 of the key columns / O columns of those rows
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float* red = reinterpret_cast<float*>(smem + S::kRed);      // [2][kAQ]
+    constexpr int kHalfK = kAK / 2;                              // 64 key columns per thread
+    constexpr int kHalfO = DP / 2;                               // O columns per thread
+    auto quad_sync = [&]() {                                      // the 2 warps sharing these rows
+      asm volatile("bar.sync %0, 64;" :: "r"(1 + quad) : "memory");
+    };
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       tc::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-      if (lane == 0 && quad == 0) ATTN_TRACE(5, 100 + j);
+      if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(5, 100 + j);
       tc::tc_fence_after();
-      float sv[kAK];
+      float sv[kHalfK];
 #pragma unroll
-      for (int c = 0; c < kAK / 32; ++c) {
+      for (int c = 0; c < kHalfK / 32; ++c) {
         uint32_t r[32];
-        tc::tmem_ld32(tmem + lane_off + (j & 1) * 128 + c * 32, r);
+        tc::tmem_ld32(tmem + lane_off + (j & 1) * 128 + half * kHalfK + c * 32, r);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) sv[c * 32 + e] = __uint_as_float(r[e]);
       }
-      const int kvalid = Lk - j * kAK;               // keys of this tile that exist
+      const int kvalid = Lk - j * kAK - half * kHalfK;   // keys of this half-tile that exist
       float mx = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < kAK; ++e) {
+      for (int e = 0; e < kHalfK; ++e) {
         sv[e] = e < kvalid ? sv[e] * scale_log2 : -INFINITY;
         mx = fmaxf(mx, sv[e]);
       }
+      red[half * kAQ + row] = mx;
+      quad_sync();
+      mx = fmaxf(red[row], red[kAQ + row]);
+      quad_sync();                                       // both read before the next tile rewrites
       const float m_new = fmaxf(m, mx);
       const float alpha = exp2f(m - m_new);
       float sum = 0.f;
@@ -230,9 +246,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         tc::mbar_wait(o_done, (j - 1) & 1);
         tc::tc_fence_after();
       }
-      if (lane == 0 && quad == 0) ATTN_TRACE(6, 100 + j);
+      if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(6, 100 + j);
 #pragma unroll
-      for (int c = 0; c < kAK / 8; ++c) {            // 16-byte chunks of the bf16 P row
+      for (int c = 0; c < kHalfK / 8; ++c) {            // 16-byte chunks of this half of the P row
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -243,22 +259,23 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
         for (int e = 0; e < 4; ++e) hp[e] = __floats2bfloat162_rn(p[2 * e], p[2 * e + 1]);
-        const int ac = c >> 3, ci = c & 7;
-        uint8_t* dst = sP + ac * (kAQ * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((ci ^ (row & 7)) << 4);
+        // this half is atom column `half` of the K-major P tile
+        uint8_t* dst = sP + half * (kAQ * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
         *reinterpret_cast<uint4*>(dst) = u;
       }
-      l = l * alpha + sum;
-      // rescale O rows whose running max moved; tcgen05.ld/st are warp-collective,
+      l = l * alpha + sum;                                // partial (this half's keys) row sum
+      // rescale this thread's half of the O row; tcgen05.ld/st are warp-collective,
       // so the whole warp takes the branch if any of its rows needs it
       if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
 #pragma unroll
-        for (int c = 0; c < DP / 32; ++c) {
+        for (int c = 0; c < kHalfO / 32; ++c) {
           uint32_t r[32];
-          tc::tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+          const uint32_t col = 256 + half * kHalfO + c * 32;
+          tc::tmem_ld32(tmem + lane_off + col, r);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(tmem + lane_off + 256 + c * 32, r);
+          tmem_st32(tmem + lane_off + col, r);
         }
         tmem_st_wait();
       }
@@ -268,21 +285,24 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full);
     }
+    red[half * kAQ + row] = l;
+    quad_sync();
+    const float lt = red[row] + red[kAQ + row];
     tc::mbar_wait(o_done, (n_tiles - 1) & 1);
-    if (lane == 0 && quad == 0) ATTN_TRACE(7, 999);
+    if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(7, 999);
     tc::tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
     const int qrow = q0 + row;
     __nv_bfloat16* orow = o + ((int64_t)b * Lq + qrow) * ldo + (int64_t)h * d;
 #pragma unroll
-    for (int c = 0; c < DP / 32; ++c) {
+    for (int c = 0; c < kHalfO / 32; ++c) {
       uint32_t r[32];
-      tc::tmem_ld32(tmem + lane_off + 256 + c * 32, r);
+      tc::tmem_ld32(tmem + lane_off + 256 + half * kHalfO + c * 32, r);
       tc::tmem_ld_wait();
       if (qrow < Lq) {
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const int col = c * 32 + e;
+          const int col = half * kHalfO + c * 32 + e;
           if (col < d)
             *reinterpret_cast<__nv_bfloat162*>(orow + col) =
                 __floats2bfloat162_rn(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv);

@@ -369,18 +369,22 @@ __global__ void gn_stats_kernel(const void* __restrict__ x, int x_f32, int HW, i
   const int n = ng / G, g = ng % G, cg = C / G;
   const int p0 = (int)((int64_t)HW * sp / kGnSplit), p1 = (int)((int64_t)HW * (sp + 1) / kGnSplit);
   const int64_t base = (int64_t)n * HW * C + (int64_t)g * cg;
-  // walk (pixel, channel) incrementally: no division in the loop
-  const int step_p = blockDim.x / cg, step_c = blockDim.x % cg;
-  int p = p0 + threadIdx.x / cg, c = threadIdx.x % cg;
+  // channel PAIRS (cg is even for every GroupNorm here): walk (pixel, pair)
+  // incrementally -- no division in the loop, 4-byte loads
+  const int cp = cg >> 1;
+  const int step_p = blockDim.x / cp, step_c = blockDim.x % cp;
+  int p = p0 + threadIdx.x / cp, c = threadIdx.x % cp;
   float s = 0.f, ss = 0.f;
   while (p < p1) {
-    const int64_t off = base + (int64_t)p * C + c;
-    const float v = x_f32 ? static_cast<const float*>(x)[off] : __bfloat162float(static_cast<const __nv_bfloat16*>(x)[off]);
-    s += v;
-    ss += v * v;
+    const int64_t off = base + (int64_t)p * C + 2 * c;
+    float2 v;
+    if (x_f32) v = *reinterpret_cast<const float2*>(static_cast<const float*>(x) + off);
+    else v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off));
+    s += v.x + v.y;
+    ss += v.x * v.x + v.y * v.y;
     c += step_c;
     p += step_p;
-    if (c >= cg) { c -= cg; ++p; }
+    if (c >= cp) { c -= cp; ++p; }
   }
   __shared__ float red[2][32];
   for (int o = 16; o; o >>= 1) {
@@ -571,7 +575,7 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
 
 extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma,
                              const float* beta, float eps, int silu, void* out, void* workspace, void* stream) {
-  if (N <= 0 || HW <= 0 || G <= 0 || C % G || C % 2 || HW % kGnPix || !gamma || !beta || !workspace)
+  if (N <= 0 || HW <= 0 || G <= 0 || C % G || (C / G) % 2 || HW % kGnPix || !gamma || !beta || !workspace)
     return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
   float2* part = static_cast<float2*>(workspace);    // N*G*kGnSplit float2

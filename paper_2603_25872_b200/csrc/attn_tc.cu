@@ -2,7 +2,7 @@
 //
 //   O[b, q, h, :] = softmax_k( Q[b, q, h, :] . K[b, k, h, :] * scale ) V[b, k, h, :]
 //
-// One CTA per (128-query tile, head, batch).  Warp roles (192 threads):
+// One CTA per (128-query tile, head, batch).  Warp roles (320 threads):
 //   warp 0      TMA producer: Q once, then K / V^T tiles of 128 keys into a
 //               kStages ring (mbarrier full/empty)
 //   warp 1      TMEM allocator + MMA issuer:  S_j = Q K_j^T   (M=128, N=128, K=DP)
@@ -15,6 +15,9 @@
 //               rescale their half of the O row only when the running max moved,
 //               write their half of P (bf16) in the UMMA SWIZZLE_128B K-major
 //               layout; the partial row sums are combined once, in the epilogue.
+//               P is double-buffered, so the exps of tile j+1 overlap PV_j; the
+//               running max only moves when a row max grows by > 2^8, so the
+//               O rescale (which must wait for PV_j) is rare.
 // Operands: Q and K through 3-D tensor maps (elem, head, row) so head dims that
 // are not multiples of 64 are zero-filled by TMA up to DP; V is consumed as V^T
 // (channels x keys, keys contiguous -- produced directly by a swapped-operand
@@ -23,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "drs_net.h"
 #include "pdl.cuh"
 #include "tc_common.cuh"
@@ -50,21 +54,34 @@ __device__ int* g_attn_trace = nullptr;
 
 template <int DP>
 struct AttnSmem {
-  static constexpr int kStages = DP <= 128 ? 2 : 1;
+  // independent softmax sets: with two, set s owns whole S rows of the key
+  // tiles j = s, s+2, ... and its own O accumulator (TMEM: S0, S1, O0, O1 =
+  // 256 + 2 DP columns <= 512); DP = 192 keeps one set whose two warps per
+  // quadrant split the key columns of every tile.
+  static constexpr int kSets = DP <= 128 ? 2 : 1;
   static constexpr int kAtoms = DP / 64;                   // 64-element K atoms of Q / K rows
-  static constexpr int kQBytes = kAQ * DP * 2;
+  static constexpr int kQBytes = kAQ * DP * 2;             // Q; reused to stage O for the TMA store
   static constexpr int kKBytes = kAK * DP * 2;
   static constexpr int kVBytes = DP * kAK * 2;
   static constexpr int kPBytes = kAQ * kAK * 2;
+  static constexpr int kRedBytes = kSets == 1 ? 2 * kAQ * 4 : 0;   // per-tile row-max exchange (1 set)
+  static constexpr int kNumBars = 26;
+  // separate K and V rings, as deep as 227 KB allows (<= 4): K_{j+s} loads as
+  // soon as S_j has consumed its slot, V_{j+s} once PV_j has
+  static constexpr int kFixed = kQBytes + 2 * kPBytes + kRedBytes + kNumBars * 8 + 1024;
+  static constexpr int kFit = (227 * 1024 - kFixed) / (kKBytes + kVBytes);
+  static constexpr int kStages = kFit > 4 ? 4 : kFit;
+  static_assert(kStages >= 1, "attention tile does not fit in shared memory");
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;
   static constexpr int kV = kK + kStages * kKBytes;
-  static constexpr int kP = kV + kStages * kVBytes;
-  static constexpr int kRed = kP + kPBytes;                // [2 halves][128 rows] float row maxima / sums
-  static constexpr int kBar = kRed + 2 * kAQ * 4;
+  static constexpr int kP = kV + kStages * kVBytes;        // P double-buffered (buffer j & 1)
+  static constexpr int kRed = kP + 2 * kPBytes;
+  static constexpr int kBar = kRed + kRedBytes;
   // >= 116 KB so two CTAs never share an SM: each allocates all 512 TMEM columns
-  static constexpr int kRaw = kBar + 16 * 8 + 16 + 1024;
+  static constexpr int kRaw = kBar + kNumBars * 8 + 1024;
   static constexpr int kBytes = kRaw < 116 * 1024 ? 116 * 1024 : kRaw;
+  static_assert(kBytes <= 227 * 1024, "shared memory plan exceeds 227 KB");
 };
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -77,7 +94,44 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
          "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
          "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
 }
+// tcgen05.wait::ld that also pins `r` (outputs of earlier tcgen05.ld) so the
+// compiler cannot move their uses above the wait
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+        "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+        "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :: "memory");
+}
+__device__ __forceinline__ void reg_pin(uint32_t (&r)[32]) {
+  asm volatile(""
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+        "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+        "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+        "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :: "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 2^x on the SFU, flush-to-zero (scores are never in the denormal range that
+// matters: p underflows to 0 exactly as the softmax wants)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA pipe (Cody-Waite split + cubic minimax on [-0.5, 0.5],
+// rel. error 7.5e-5, far below P's bf16 rounding): used for some of the
+// scores so the SFU is not the only exp2 engine
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);                            // keeps the result a normal float (masked -inf -> ~0)
+  const float t = x + 12582912.f;                  // 1.5 * 2^23: round to nearest integer
+  const float r = t - 12582912.f;
+  const float f = x - r;                           // [-0.5, 0.5]
+  float p = fmaf(fmaf(fmaf(0.0551715f, f, 0.24261096f), f, 0.69326099f), f, 0.99992808f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2) {
@@ -91,23 +145,39 @@ __device__ __forceinline__ uint64_t kdesc(const uint8_t* base, int kk, int atom_
   return tc::smem_desc_sw128(base + (kk >> 2) * atom_bytes + (kk & 3) * 32);
 }
 
-template <int DP>
+__device__ __forceinline__ void tma_store_4d(const void* tmap, const void* smem, int32_t c0, int32_t c1, int32_t c2,
+                                             int32_t c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+               :: "l"(tmap), "r"(tc::smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+
+// byte offset of the 16-byte chunk holding columns [8c, 8c+8) of `row` in a
+// 128-row tile stored as 64-column SWIZZLE_128B atoms (UMMA K-major / TMA layout)
+__device__ __forceinline__ int sw128_off(int row, int c) {
+  return (c >> 3) * (kAQ * 128) + (row >> 3) * 1024 + (row & 7) * 128 + (((c & 7) ^ (row & 7)) << 4);
+}
+
+template <int DP, int NPOLY>
 __global__ void __launch_bounds__(kAttnTcThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_vt, __nv_bfloat16* __restrict__ o, int64_t ldo,
+               const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
                int Lq, int Lk, int d, int vt_img, float scale_log2) {
   using S = AttnSmem<DP>;
   constexpr int kSt = S::kStages;
+  constexpr int kSets = S::kSets;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* q_full = bars;                 // 1
-  uint64_t* kv_full = bars + 1;            // kSt
-  uint64_t* kv_empty = bars + 3;           // kSt
-  uint64_t* s_full = bars + 5;             // 2 (per S buffer)
-  uint64_t* p_full = bars + 7;             // 1 (count 8: softmax warps)
-  uint64_t* o_done = bars + 8;             // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars + 1;             // kSt (<= 4)
+  uint64_t* k_empty = bars + 5;            // kSt   (released by S_j)
+  uint64_t* v_full = bars + 9;             // kSt
+  uint64_t* v_empty = bars + 13;           // kSt   (released by PV_j)
+  uint64_t* s_full = bars + 17;            // 2 (per S buffer)
+  uint64_t* p_full = bars + 19;            // 2 (per P buffer; one arrival per softmax warp of the tile)
+  uint64_t* o_done = bars + 21;            // 2 (per P buffer: PV_j committed to o_done[j & 1])
+  uint64_t* s_free = bars + 23;            // 2 (S buffer read into registers: S_{j+2} may overwrite)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * kAQ, h = blockIdx.y, b = blockIdx.z;
@@ -119,12 +189,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     tc::tma_prefetch(&tm_q);
     tc::tma_prefetch(&tm_k);
     tc::tma_prefetch(&tm_vt);
+    tc::tma_prefetch(&tm_o);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < kSt; ++s) { tc::mbar_init(&kv_full[s], 1); tc::mbar_init(&kv_empty[s], 1); }
-    tc::mbar_init(&s_full[0], 1);
-    tc::mbar_init(&s_full[1], 1);
-    tc::mbar_init(p_full, 8);
-    tc::mbar_init(o_done, 1);
+    for (int s = 0; s < kSt; ++s) {
+      tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1);
+      tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&p_full[i], kSets == 2 ? 4 : 8);
+      tc::mbar_init(&s_free[i], kSets == 2 ? 4 : 8);
+      tc::mbar_init(&o_done[i], 1);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
@@ -133,7 +209,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   tc::tc_fence_after();
   pdl_wait();       // everything above is data-independent setup (PDL overlap)
   pdl_trigger();
-  const uint32_t tmem = *tmem_slot;         // S0 at col 0, S1 at col 128, O at col 256
+  const uint32_t tmem = *tmem_slot;         // S0 at col 0, S1 at col 128, O (per set) from col 256
   if (threadIdx.x == 0) ATTN_TRACE(0, 1);
   uint8_t* sQ = smem + S::kQ;
   uint8_t* sK = smem + S::kK;
@@ -141,32 +217,39 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint8_t* sP = smem + S::kP;
 
   if (warp == 0) {
-    if (tc::elect_one()) {
+    // two producer lanes: lane 0 streams Q then the K ring, lane 1 the V ring
+    if (lane == 0) {
       tc::mbar_arrive_expect_tx(q_full, S::kQBytes);
       for (int a = 0; a < S::kAtoms; ++a)
         tma_load_3d(&tm_q, q_full, sQ + a * (kAQ * 128), a * 64, h, b * Lq + q0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % kSt;
-        const uint32_t ph = (j / kSt) & 1;
-        tc::mbar_wait(&kv_empty[st], ph ^ 1);
+        tc::mbar_wait(&k_empty[st], ((j / kSt) & 1) ^ 1);
         ATTN_TRACE(1, 100 + j);
-        tc::mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
+        tc::mbar_arrive_expect_tx(&k_full[st], S::kKBytes);
         uint8_t* k_dst = sK + st * S::kKBytes;
-        uint8_t* v_dst = sV + st * S::kVBytes;
         for (int a = 0; a < S::kAtoms; ++a)
-          tma_load_3d(&tm_k, &kv_full[st], k_dst + a * (kAK * 128), a * 64, h, b * Lk + j * kAK);
+          tma_load_3d(&tm_k, &k_full[st], k_dst + a * (kAK * 128), a * 64, h, b * Lk + j * kAK);
+      }
+    } else if (lane == 1) {
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % kSt;
+        tc::mbar_wait(&v_empty[st], ((j / kSt) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&v_full[st], S::kVBytes);
+        uint8_t* v_dst = sV + st * S::kVBytes;
         for (int a = 0; a < kAK / 64; ++a)
-          tc::tma_load_2d(&tm_vt, &kv_full[st], v_dst + a * (DP * 128), b * vt_img + j * kAK + a * 64, h * d);
+          tc::tma_load_2d(&tm_vt, &v_full[st], v_dst + a * (DP * 128), b * vt_img + j * kAK + a * 64, h * d);
       }
     }
   } else if (warp == 1) {
-    // S_j = Q K_j^T into TMEM buffer j&1; O += P_j V_j after the softmax publishes P_j.
-    if (lane == 0) ATTN_TRACE(2, 5);
+    // S_j = Q K_j^T into TMEM buffer j&1 (S_0, S_1 up front, S_{j+2} as soon as
+    // the softmax has read S_j into registers, so it runs under tile j's exps);
+    // O_set += P_j V_j after P_j is published.
     tc::mbar_wait(q_full, 0);
     if (lane == 0) ATTN_TRACE(2, 6);
     auto issue_s = [&](int j) {
       const int st = j % kSt;
-      tc::mbar_wait(&kv_full[st], (j / kSt) & 1);
+      tc::mbar_wait(&k_full[st], (j / kSt) & 1);
       if (lane == 0) ATTN_TRACE(3, 100 + j);
       tc::tc_fence_after();
       if (tc::elect_one()) {
@@ -175,104 +258,133 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (int kk = 0; kk < DP / 16; ++kk)
           tc::mma_bf16(tmem + (j & 1) * 128, kdesc(sQ, kk, kAQ * 128), kdesc(kb, kk, kAK * 128), kIdescS,
                        kk > 0 ? 1u : 0u);
+        tc::mma_commit(&k_empty[st]);
         tc::mma_commit(&s_full[j & 1]);
       }
       __syncwarp();
     };
     issue_s(0);
+    if (n_tiles > 1) issue_s(1);
     for (int j = 0; j < n_tiles; ++j) {
-      // with a 2-deep K/V ring S_{j+1} overlaps the softmax of tile j; with one
-      // stage it must wait until PV_j has released the ring slot
-      if (kSt > 1 && j + 1 < n_tiles) issue_s(j + 1);
-      tc::mbar_wait(p_full, j & 1);
+      if (j + 2 < n_tiles) {
+        tc::mbar_wait(&s_free[j & 1], (j >> 1) & 1);
+        issue_s(j + 2);
+      }
+      tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      const int st = j % kSt;
+      tc::mbar_wait(&v_full[st], (j / kSt) & 1);
       if (lane == 0) ATTN_TRACE(4, 100 + j);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const int st = j % kSt;
         const uint8_t* vb = sV + st * S::kVBytes;
+        const uint32_t o_col = 256 + (kSets == 2 ? (j & 1) * DP : 0);
 #pragma unroll
         for (int kk = 0; kk < kAK / 16; ++kk)
-          tc::mma_bf16(tmem + 256, kdesc(sP, kk, kAQ * 128), kdesc(vb, kk, DP * 128), kIdescO,
-                       (j > 0 || kk > 0) ? 1u : 0u);
-        tc::mma_commit(&kv_empty[st]);
-        tc::mma_commit(o_done);
+          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), kdesc(vb, kk, DP * 128),
+                       kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&v_empty[st]);
+        tc::mma_commit(&o_done[j & 1]);
       }
       __syncwarp();
-      if (kSt == 1 && j + 1 < n_tiles) issue_s(j + 1);
     }
   } else {
-    // softmax warps: warp w owns TMEM lanes 32*(w&3) .. +31 (query rows) and
-    // the half (w-2)>>2 of the key columns / O columns of those rows
+    // softmax warps: warp w owns TMEM lanes 32*(w&3) .. +31 (query rows);
+    // grp = (w-2)>>2 is the set (2 sets) or the key-column half (1 set)
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int grp = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    float* red = reinterpret_cast<float*>(smem + S::kRed);      // [2][kAQ]
-    constexpr int kHalfK = kAK / 2;                              // 64 key columns per thread
-    constexpr int kHalfO = DP / 2;                               // O columns per thread
+    constexpr int kCols = kSets == 2 ? kAK : kAK / 2;            // S columns per thread per tile
+    const int col0 = kSets == 2 ? 0 : grp * kCols;
+    const uint32_t o_base = 256 + (kSets == 2 ? grp * DP : grp * (DP / 2));
+    constexpr int kOCols = kSets == 2 ? DP : DP / 2;              // O columns rescaled per thread
+    float* red = reinterpret_cast<float*>(smem + S::kRed);       // [2][kAQ] (1 set only)
     auto quad_sync = [&]() {                                      // the 2 warps sharing these rows
       asm volatile("bar.sync %0, 64;" :: "r"(1 + quad) : "memory");
     };
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
+    for (int j = (kSets == 2 ? grp : 0); j < n_tiles; j += kSets) {
       tc::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-      if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(5, 100 + j);
+      if (lane == 0 && quad == 0) ATTN_TRACE(5 + grp, 100 + j);
       tc::tc_fence_after();
-      float sv[kHalfK];
+      float sv[kCols];
+      {                                                   // all chunks in flight, one wait
+        uint32_t r[kCols / 32][32];
 #pragma unroll
-      for (int c = 0; c < kHalfK / 32; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld32(tmem + lane_off + (j & 1) * 128 + half * kHalfK + c * 32, r);
-        tc::tmem_ld_wait();
+        for (int c = 0; c < kCols / 32; ++c) tc::tmem_ld32(tmem + lane_off + (j & 1) * 128 + col0 + c * 32, r[c]);
+        tmem_ld_wait_regs(r[0]);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) sv[c * 32 + e] = __uint_as_float(r[e]);
+        for (int c = 1; c < kCols / 32; ++c) reg_pin(r[c]);
+#pragma unroll
+        for (int c = 0; c < kCols / 32; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sv[c * 32 + e] = __uint_as_float(r[c][e]);
       }
-      const int kvalid = Lk - j * kAK - half * kHalfK;   // keys of this half-tile that exist
-      float mx = -INFINITY;
+      tc::tc_fence_before();                              // S_j is in registers: release the buffer
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_free[j & 1]);
+      const int kvalid = Lk - j * kAK - col0;             // keys of this (half-)tile that exist
+      if (kvalid < kCols) {                               // ragged last tile only
 #pragma unroll
-      for (int e = 0; e < kHalfK; ++e) {
-        sv[e] = e < kvalid ? sv[e] * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sv[e]);
+        for (int e = 0; e < kCols; ++e) sv[e] = e < kvalid ? sv[e] : -INFINITY;
       }
-      red[half * kAQ + row] = mx;
-      quad_sync();
-      mx = fmaxf(red[row], red[kAQ + row]);
-      quad_sync();                                       // both read before the next tile rewrites
-      const float m_new = fmaxf(m, mx);
-      const float alpha = exp2f(m - m_new);
-      float sum = 0.f;
-      // P_j overwrites the P buffer and O may be rescaled: PV_{j-1} must be done
-      if (j > 0) {
-        tc::mbar_wait(o_done, (j - 1) & 1);
+      float mx8[8];                                       // max tree on the raw scores (scale > 0)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(sv[e], sv[e + 8]);
+#pragma unroll
+      for (int c = 2; c < kCols / 8; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(mx8[e], sv[c * 8 + e]);
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+      if constexpr (kSets == 1) {
+        red[grp * kAQ + row] = mx;
+        quad_sync();
+        mx = fmaxf(red[row], red[kAQ + row]);
+        quad_sync();                                     // both read before the next tile rewrites
+      }
+      // conditional rescaling: the reference max only moves when the row max
+      // grew by more than 2^8 (p <= 256 is exact enough for bf16 P / fp32 l;
+      // the final O / l uses the same stale max for both, so the result is unchanged)
+      const float m_new = mx > m + 8.f ? mx : m;
+      const float alpha = ex2(m - m_new);
+      // P_j overwrites P buffer j&1: PV_{j-2} (its last reader) must be done.
+      // With two sets that PV is also the last one into this set's O.
+      if (j >= 2) {
+        tc::mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
         tc::tc_fence_after();
       }
-      if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(6, 100 + j);
+      uint8_t* pb = sP + (j & 1) * S::kPBytes;
+      float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < kHalfK / 8; ++c) {            // 16-byte chunks of this half of the P row
+      for (int c = 0; c < kCols / 8; ++c) {            // 16-byte chunks of this thread's P row
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          p[e] = exp2f(sv[c * 8 + e] - m_new);
-          sum += p[e];
+          const float x = fmaf(sv[c * 8 + e], scale_log2, -m_new);
+          p[e] = e < NPOLY ? ex2_poly(x) : ex2(x);      // NPOLY of every 8 on the FMA pipe
         }
+        sum += ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
         uint4 u;
         __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
         for (int e = 0; e < 4; ++e) hp[e] = __floats2bfloat162_rn(p[2 * e], p[2 * e + 1]);
-        // this half is atom column `half` of the K-major P tile
-        uint8_t* dst = sP + half * (kAQ * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = u;
+        *reinterpret_cast<uint4*>(pb + sw128_off(row, (col0 >> 3) + c)) = u;
       }
-      l = l * alpha + sum;                                // partial (this half's keys) row sum
-      // rescale this thread's half of the O row; tcgen05.ld/st are warp-collective,
+      l = l * alpha + sum;                                // this thread's (partial) row sum
+      // rescale this thread's O columns; tcgen05.ld/st are warp-collective,
       // so the whole warp takes the branch if any of its rows needs it
-      if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+      if (j >= kSets && __any_sync(0xffffffffu, alpha < 1.f)) {
+        if constexpr (kSets == 1) {
+          tc::mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);   // O holds PV_0..PV_{j-1}
+          tc::tc_fence_after();
+        }
 #pragma unroll
-        for (int c = 0; c < kHalfO / 32; ++c) {
+        for (int c = 0; c < kOCols / 32; ++c) {
           uint32_t r[32];
-          const uint32_t col = 256 + half * kHalfO + c * 32;
+          const uint32_t col = o_base + c * 32;
           tc::tmem_ld32(tmem + lane_off + col, r);
-          tc::tmem_ld_wait();
+          tmem_ld_wait_regs(r);
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
           tmem_st32(tmem + lane_off + col, r);
@@ -283,31 +395,80 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       fence_async_smem();                            // P smem writes -> tensor-core (async) proxy
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
+      if (lane == 0) tc::mbar_arrive(&p_full[j & 1]);
     }
-    red[half * kAQ + row] = l;
-    quad_sync();
-    const float lt = red[row] + red[kAQ + row];
-    tc::mbar_wait(o_done, (n_tiles - 1) & 1);
-    if (lane == 0 && quad == 0 && half == 0) ATTN_TRACE(7, 999);
+
+    // ---- epilogue: O / l -> bf16, staged in the (dead) Q tile, TMA-stored ----
+    // wait for the last PV this thread's set (or, with one set, the CTA) issued
+    float f0 = 1.f, f1 = 0.f, inv;
+    if constexpr (kSets == 2) {
+      const int last = n_tiles - 1 - ((n_tiles - 1 - grp) & 1);   // last tile of this set (may be < 0)
+      if (last >= 0) {
+        tc::mbar_wait(&o_done[grp], (last >> 1) & 1);
+        tc::tc_fence_after();
+      }
+      // this set's P buffer is now dead: publish (m, l) of the row through it
+      float* ex = reinterpret_cast<float*>(sP + grp * S::kPBytes);
+      ex[row] = m;
+      ex[kAQ + row] = l;
+      quad_sync();
+      const float* ex0 = reinterpret_cast<const float*>(sP);
+      const float* ex1 = reinterpret_cast<const float*>(sP + S::kPBytes);
+      const float m0 = ex0[row], l0 = ex0[kAQ + row], m1 = ex1[row], l1 = ex1[kAQ + row];
+      const float mm = fmaxf(m0, m1);
+      f0 = ex2(m0 - mm);
+      f1 = n_tiles > 1 ? ex2(m1 - mm) : 0.f;
+      const float lt = l0 * f0 + l1 * f1;
+      inv = lt > 0.f ? 1.f / lt : 0.f;
+    } else {
+      tc::mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+      tc::tc_fence_after();
+      red[grp * kAQ + row] = l;
+      quad_sync();
+      const float lt = red[row] + red[kAQ + row];
+      inv = lt > 0.f ? 1.f / lt : 0.f;
+    }
     tc::tc_fence_after();
-    const float inv = lt > 0.f ? 1.f / lt : 0.f;
-    const int qrow = q0 + row;
-    __nv_bfloat16* orow = o + ((int64_t)b * Lq + qrow) * ldo + (int64_t)h * d;
+    // this thread writes O columns [grp * DP/2, (grp+1) * DP/2) of its row
+    constexpr int kHalfO = DP / 2;
 #pragma unroll
     for (int c = 0; c < kHalfO / 32; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + lane_off + 256 + half * kHalfO + c * 32, r);
-      tc::tmem_ld_wait();
-      if (qrow < Lq) {
+      const int ocol = grp * kHalfO + c * 32;
+      uint32_t r0[32];
+      tc::tmem_ld32(tmem + lane_off + 256 + ocol, r0);
+      if (kSets == 2 && n_tiles > 1) {
+        uint32_t r1[32];
+        tc::tmem_ld32(tmem + lane_off + 256 + DP + ocol, r1);
+        tmem_ld_wait_regs(r0);
+        reg_pin(r1);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = half * kHalfO + c * 32 + e;
-          if (col < d)
-            *reinterpret_cast<__nv_bfloat162*>(orow + col) =
-                __floats2bfloat162_rn(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv);
+        for (int e = 0; e < 32; ++e)
+          r0[e] = __float_as_uint(fmaf(__uint_as_float(r0[e]), f0, __uint_as_float(r1[e]) * f1));
+      } else {
+        tmem_ld_wait_regs(r0);
+        if (kSets == 2) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r0[e] = __float_as_uint(__uint_as_float(r0[e]) * f0);
         }
       }
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint4 u;
+        __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          hp[e] = __floats2bfloat162_rn(__uint_as_float(r0[c8 * 8 + 2 * e]) * inv,
+                                        __uint_as_float(r0[c8 * 8 + 2 * e + 1]) * inv);
+        *reinterpret_cast<uint4*>(sQ + sw128_off(row, (ocol >> 3) + c8)) = u;
+      }
+    }
+    fence_async_smem();
+    asm volatile("bar.sync 5, 256;" ::: "memory");        // all softmax warps staged their O
+    if (warp == 2 && lane == 0) {
+      for (int a = 0; a < S::kAtoms; ++a) tma_store_4d(&tm_o, sQ + a * (kAQ * 128), a * 64, h, q0, b);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem must outlive the reads
+      ATTN_TRACE(7, 999);
     }
   }
   tc::tc_fence_before();
@@ -345,6 +506,20 @@ static bool tmap_heads(CUtensorMap* m, const void* ptr, int64_t rows, int H, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// output (elements of a head, heads, queries, images): box {64, 1, 128, 1}; the
+// TMA store clips elements >= d and queries >= Lq (no spill into the next image)
+static bool tmap_out(CUtensorMap* m, void* ptr, int B, int Lq, int H, int d, int64_t ld) {
+  auto enc = encode_fn2();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)Lq, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)ld * 2, (cuuint64_t)Lq * ld * 2};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 // V^T (channels x keys): box {64 keys, DP channels}
 static bool tmap_vt(CUtensorMap* m, const void* ptr, int64_t chans, int64_t keys, int64_t ld, int DP) {
   auto enc = encode_fn2();
@@ -358,11 +533,11 @@ static bool tmap_vt(CUtensorMap* m, const void* ptr, int64_t chans, int64_t keys
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DP>
-static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, void* o, int64_t ldo,
-                       int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
+template <int DP, int NPOLY>
+static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
+                         int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   using S = AttnSmem<DP>;
-  auto kern = attn_tc_kernel<DP>;
+  auto kern = attn_tc_kernel<DP, NPOLY>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
@@ -370,9 +545,17 @@ static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
     attr = true;
   }
   dim3 grid((Lq + kAQ - 1) / kAQ, H, B);
-  launch_pdl(kern, dim3(grid), dim3(kAttnTcThreads), S::kBytes, st, tq, tk, tv, static_cast<__nv_bfloat16*>(o), ldo, Lq, Lk, d, vt_img,
-                                                sl2);
+  launch_pdl(kern, dim3(grid), dim3(kAttnTcThreads), S::kBytes, st, tq, tk, tv, to, Lq, Lk, d, vt_img, sl2);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+template <int DP>
+static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
+                       int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
+  static int npoly = [] { const char* e = getenv("DRS_ATTN_POLY"); return e ? atoi(e) : 2; }();
+  if (npoly == 0) return launch_attn_v<DP, 0>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (npoly == 3) return launch_attn_v<DP, 3>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  return launch_attn_v<DP, 2>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
 }
 
 }  // namespace drs
@@ -383,19 +566,20 @@ extern "C" int drs_attention_tc(const void* q, int64_t ldq, const void* k, int64
   using namespace drs;
   if (B <= 0 || H <= 0 || Lq <= 0 || Lk <= 0 || d <= 0 || d > 192 || d % 8) return DRS_ERR_VALUE;
   if (vt_img < Lk || vt_img % 8) return DRS_ERR_VALUE;   // TMA inner box starts must be 16-byte aligned
-  if ((ldq | ldk | ldvt) % 8 || (reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
-                                 reinterpret_cast<uintptr_t>(vt)) & 15)
+  if ((ldq | ldk | ldvt | ldo) % 8 || (reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+                                       reinterpret_cast<uintptr_t>(vt) | reinterpret_cast<uintptr_t>(o)) & 15)
     return DRS_ERR_VALUE;
   const int DP = d <= 64 ? 64 : (d <= 128 ? 128 : 192);
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, to;
   if (!tmap_heads(&tq, q, (int64_t)B * Lq, H, d, ldq) || !tmap_heads(&tk, k, (int64_t)B * Lk, H, d, ldk) ||
-      !tmap_vt(&tv, vt, (int64_t)H * d, (int64_t)(B - 1) * vt_img + Lk, ldvt, DP))
+      !tmap_vt(&tv, vt, (int64_t)H * d, (int64_t)(B - 1) * vt_img + Lk, ldvt, DP) ||
+      !tmap_out(&to, o, B, Lq, H, d, ldo))
     return DRS_ERR_CUDA;
   const float sl2 = scale * 1.4426950408889634f;
   cudaStream_t st = (cudaStream_t)stream;
-  if (DP == 64) return launch_attn<64>(tq, tk, tv, o, ldo, B, H, Lq, Lk, d, vt_img, sl2, st);
-  if (DP == 128) return launch_attn<128>(tq, tk, tv, o, ldo, B, H, Lq, Lk, d, vt_img, sl2, st);
-  return launch_attn<192>(tq, tk, tv, o, ldo, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (DP == 64) return launch_attn<64>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (DP == 128) return launch_attn<128>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  return launch_attn<192>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
 }
 
 extern "C" int drs_attention_tc_debug(int* mapped_trace) {

@@ -106,21 +106,26 @@ def test_sd15_unet_vs_torch_fp32(cuda, size, g):
     assert net.flops > 0
 
 
-@pytest.mark.parametrize("B,H,Lq,Lk,d", [(1, 16, 256, 256, 72), (2, 8, 1024, 77, 40), (1, 5, 300, 300, 64),
-                                         (2, 8, 4096, 4096, 40), (1, 8, 128, 200, 160), (1, 2, 70, 33, 80),
-                                         (2, 10, 1024, 1024, 64)])
-def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d):
-    """tcgen05 attention (V given transposed) vs torch fp32."""
+@pytest.mark.parametrize("B,H,Lq,Lk,d,amp", [(1, 16, 256, 256, 72, 1), (2, 8, 1024, 77, 40, 1), (1, 5, 300, 300, 64, 1),
+                                             (2, 8, 4096, 4096, 40, 1), (1, 8, 128, 200, 160, 1), (1, 2, 70, 33, 80, 1),
+                                             (2, 10, 1024, 1024, 64, 1), (3, 4, 70, 300, 160, 1),
+                                             (3, 3, 200, 333, 96, 1), (2, 8, 64, 64, 160, 1), (2, 2, 129, 1, 64, 1),
+                                             (2, 4, 256, 700, 64, 6), (2, 4, 256, 700, 160, 6)])
+def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d, amp):
+    """tcgen05 attention (V given transposed) vs torch fp32; amp > 1 sharpens the
+    softmax so the running max moves across key tiles (O rescaling)."""
     from paper_2603_25872_b200.netops import attention_tc
     g = torch.Generator(device=cuda).manual_seed(Lq + d + 1)
-    q = torch.randn(B * Lq, 3 * H * d, device=cuda, generator=g).bfloat16()
+    q = (amp * torch.randn(B * Lq, 3 * H * d, device=cuda, generator=g)).bfloat16()
     k = torch.randn(B * Lk, 2 * H * d, device=cuda, generator=g).bfloat16()
     v = torch.randn(B * Lk, H * d, device=cuda, generator=g).bfloat16()
     vimg = (Lk + 7) // 8 * 8                          # TMA: 16-byte aligned per-image key blocks
     vt = torch.zeros(H * d, B * vimg, device=cuda, dtype=torch.bfloat16)
     for b in range(B):
         vt[:, b * vimg:b * vimg + Lk] = v[b * Lk:(b + 1) * Lk].t()
-    out = torch.zeros(B * Lq, H * d, device=cuda, dtype=torch.bfloat16)
+    # output rows beyond B*Lq hold a sentinel the kernel must not touch
+    full = torch.full((B * Lq + 130, H * d), 7.0, device=cuda, dtype=torch.bfloat16)
+    out = full[:B * Lq]
     attention_tc(q[:, :H * d], k[:, :H * d], vt, out, B, H, Lq, Lk, d, vt_img=vimg)
     Q = q[:, :H * d].float().reshape(B, Lq, H, d).transpose(1, 2)
     K = k[:, :H * d].float().reshape(B, Lk, H, d).transpose(1, 2)
@@ -128,3 +133,4 @@ def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d):
     ref = (torch.softmax(Q @ K.transpose(-1, -2) / math.sqrt(d), -1) @ V).transpose(1, 2).reshape(B * Lq, H * d)
     rel = ((out.float() - ref).norm() / ref.norm()).item()
     assert rel < 1e-2, rel
+    assert bool((full[B * Lq:] == 7.0).all())

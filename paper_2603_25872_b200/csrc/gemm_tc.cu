@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <string.h>
 #include "drs_net.h"
 #include "pdl.cuh"
 #include "tc_common.cuh"
@@ -56,42 +57,75 @@ struct EpiParams {
   int act;                  // DRS_ACT_*
   int out_f32;              // 1: fp32 output, 0: bf16
   float* partial;           // split-K workspace [split][M][N] fp32 (split > 1)
+  int tma_store;            // 1: output written through smem staging + TMA (tmap_c)
 };
 
-// Apply the epilogue to 32 consecutive accumulator columns n0..n0+31 of `row`.
-__device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
-  if (row >= M) return;
-  const float* rb = p.rowbias ? p.rowbias + (int64_t)(row / p.rb_group) * p.rb_ld : nullptr;
+// Epilogue math on 32 consecutive accumulator columns n0..n0+31 of `row`:
+// alpha, bias, row bias, activation (GEGLU folds (value, gate) pairs into 16
+// outputs), column gate, residual.  Returns the number of outputs now in v[]
+// (32, or 16 for GEGLU; output column of v[0] = n0 or n0 / 2).  Rows >= M
+// compute garbage without touching memory (the TMA store clips them).
+__device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
+  const bool row_ok = row < M;
+  const bool full = n0 + 32 <= N;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int n = n0 + j;
-    float x = v[j] * p.alpha;
-    if (p.bias && n < N) x += __ldg(p.bias + n);
-    if (rb && n < N) x += __ldg(rb + n);
-    v[j] = x;
+  for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+  if (p.bias) {
+    if (full && ((reinterpret_cast<uintptr_t>(p.bias + n0) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(p.bias + n0) + q);
+        v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(p.bias + n0 + j);
+    }
+  }
+  if (p.rowbias && row_ok) {
+    const float* rb = p.rowbias + (int64_t)(row / p.rb_group) * p.rb_ld + n0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(rb + j);
   }
   if (p.act == DRS_ACT_GEGLU) {                // interleaved (value, gate) pairs -> N/2 outputs
-    float o[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
+    for (int j = 0; j < 16; ++j) v[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
     const int c0 = n0 / 2;
-    if (p.res) {
+    const bool gfull = c0 + 16 <= N / 2;
+    if (p.res && row_ok) {
+      if (p.res_f32) {
+        const float* r = static_cast<const float*>(p.res) + (int64_t)row * p.ldr + c0;
+        if (gfull && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < N / 2)
-          o[j] += p.res_f32 ? static_cast<const float*>(p.res)[(int64_t)row * p.ldr + c0 + j]
-                            : __bfloat162float(static_cast<const __nv_bfloat16*>(p.res)[(int64_t)row * p.ldr + c0 + j]);
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = *reinterpret_cast<const float4*>(r + 4 * q);
+            v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) v[j] += r[j];
+        }
+      } else {
+        const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.res) + (int64_t)row * p.ldr + c0;
+        if (gfull && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint4 u = *reinterpret_cast<const uint4*>(r + 8 * q);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              v[8 * q + 2 * e] += f.x;
+              v[8 * q + 2 * e + 1] += f.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) v[j] += __bfloat162float(r[j]);
+        }
+      }
     }
-    if (p.out_f32) {
-      float* dst = static_cast<float*>(p.out) + (int64_t)row * p.ldo + c0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) dst[j] = o[j];
-    } else {
-      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ldo + c0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) dst[j] = __float2bfloat16(o[j]);
-    }
-    return;
+    return 16;
   }
   if (p.act == DRS_ACT_GELU_TANH) {
 #pragma unroll
@@ -103,13 +137,12 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
   }
-  const bool full = n0 + 32 <= N;
-  if (p.colscale) {
+  if (p.colscale && row_ok) {
     const float* cs = p.colscale + (p.cs_group > 0 ? (int64_t)(row / p.cs_group) * p.cs_ld : 0) + n0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] *= __ldg(cs + j);
   }
-  if (p.res && p.res_f32) {
+  if (p.res && row_ok && p.res_f32) {
     const float* r = static_cast<const float*>(p.res) + (int64_t)row * p.ldr + n0;
     if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
@@ -121,7 +154,7 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int
 #pragma unroll
       for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += r[j];
     }
-  } else if (p.res) {
+  } else if (p.res && row_ok) {
     const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.res) + (int64_t)row * p.ldr + n0;
     if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
@@ -140,33 +173,86 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int
       for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __bfloat162float(r[j]);
     }
   }
+  return 32;
+}
+
+// Direct (per-row) store of the nout outputs of epi_math32 at output column c0.
+__device__ __forceinline__ void epi_store_direct(const EpiParams& p, int M, int n_out, int row, int c0, int nout,
+                                                 const float (&v)[32]) {
+  if (row >= M) return;
+  const bool full = c0 + nout <= n_out;
   if (p.out_f32) {
-    float* dst = static_cast<float*>(p.out) + (int64_t)row * p.ldo + n0;
+    float* dst = static_cast<float*>(p.out) + (int64_t)row * p.ldo + c0;
     if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (4 * q < nout)
+          *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = v[j];
+      for (int j = 0; j < 32; ++j) if (j < nout && c0 + j < n_out) dst[j] = v[j];
     }
   } else {
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ldo + n0;
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.ldo + c0;
     if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint4 u;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+        if (8 * q < nout) {
+          uint4 u;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-        *reinterpret_cast<uint4*>(dst + 8 * q) = u;
+          for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(dst + 8 * q) = u;
+        }
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = __float2bfloat16(v[j]);
+      for (int j = 0; j < 32; ++j) if (j < nout && c0 + j < n_out) dst[j] = __float2bfloat16(v[j]);
     }
   }
 }
+
+__device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
+  const int nout = epi_math32(p, M, N, row, n0, v);
+  const bool geglu = nout == 16;
+  epi_store_direct(p, M, geglu ? N / 2 : N, row, geglu ? n0 / 2 : n0, nout, v);
+}
+
+// Staged store: this warp's 32 rows x nout outputs go to a 32-row smem tile
+// (row pitch = nout * elem bytes = 32 / 64 / 128 B, TMA swizzle of the same
+// span: 16-byte chunk index ^= bits 7.. of the byte offset), then one TMA
+// bulk-tensor store writes the coalesced block; out-of-range rows / columns
+// are clipped by the tensor map.
+__device__ __forceinline__ void stage_rows(uint8_t* buf, int lane, int pitch, bool f32, const float (&v)[32]) {
+  const int mask = pitch == 128 ? 7 : (pitch == 64 ? 3 : 1);
+  const int nchunk = pitch / 16;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q < nchunk) {
+      uint4 u;
+      if (f32) {
+        u = make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
+                       __float_as_uint(v[4 * q + 3]));
+      } else {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+      }
+      const int off = lane * pitch + q * 16;
+      *reinterpret_cast<uint4*>(buf + (off ^ (((off >> 7) & mask) << 4))) = u;
+    }
+  }
+}
+
+__device__ __forceinline__ void fence_async_smem_g() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :: "l"(tmap), "r"(tc::smem_u32(smem)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Implicit-GEMM 3x3 convolution (stride 1, pad 1) over an NHWC bf16 input:
 // A[(n,y,x), (ky,kx,c)] is never materialised -- the k-block (tap, 64-channel
@@ -188,19 +274,24 @@ __device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, voi
       : "memory");
 }
 
+constexpr int kStgBytes = 4096;        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
+
 template <int BN, int kStages>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBarOffset = kStages * kStageBytes;
+  static constexpr int kStgOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
   static constexpr int kBytes = kBarOffset + (2 * kStages + 4) * 8 + 16 + 1024;   // +1024 alignment slack
+  static_assert(kBytes <= 227 * 1024, "GEMM shared memory plan exceeds 227 KB");
 };
 
 template <int BN, int kStages>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    int M, int N, int K, int split, EpiParams ep, ConvGeom cv) {
+                    const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K, int split, EpiParams ep,
+                    ConvGeom cv) {
   using S = GemmSmem<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -221,6 +312,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmap_a);
     tc::tma_prefetch(&tmap_b);
+    if (ep.tma_store) tc::tma_prefetch(&tmap_c);
     for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
     for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], kEpiWarps); }
     tc::fence_barrier_init();
@@ -302,6 +394,11 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     // ---------------- epilogue (warps 2..9) ----------------
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
     const int half = (warp - 2) >> 2;              // which 32-column chunks (even / odd) it drains
+    const bool geglu = ep.act == DRS_ACT_GEGLU;
+    const int pitch = (geglu ? 16 : 32) * (ep.out_f32 ? 4 : 2);   // staged row bytes
+    const bool dbl = pitch * 32 <= kStgBytes / 2;                 // two staging buffers fit
+    uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
+    int buf = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int sp = tile % split;
@@ -329,6 +426,22 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
 #pragma unroll
             for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = v[j];
           }
+        } else if (ep.tma_store) {
+          epi_math32(ep, M, N, row, n0, v);
+          // the buffer about to be written must have been read by its last store
+          if (lane == 0) {
+            if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          }
+          __syncwarp();
+          uint8_t* sb = stg + buf * (kStgBytes / 2);
+          stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
+          fence_async_smem_g();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_c, sb, geglu ? n0 / 2 : n0, mt * kBM + quad * 32);
+            bulk_commit();
+          }
+          if (dbl) buf ^= 1;
         } else {
           epilogue32(ep, M, N, row, n0, v);
         }
@@ -337,6 +450,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty_bar[acc]);
     }
+    if (ep.tma_store && lane == 0) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem_base);
@@ -417,6 +531,23 @@ static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output map for the staged TMA store: {n_out cols, M rows}, box {cols_box, 32}
+// with the swizzle whose span equals the staged row pitch (32 / 64 / 128 B).
+static bool make_tmap_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, int elem, int cols_box) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const int pitch = cols_box * elem;
+  const CUtensorMapSwizzle sw = pitch == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : (pitch == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * elem)};
+  cuuint32_t box[2] = {(cuuint32_t)cols_box, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -428,8 +559,8 @@ static int num_sms() {
 }
 
 template <int BN, int kStages>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
-                       const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, int M, int N, int K,
+                       int split, const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
   auto kern = gemm_bf16_tc_kernel<BN, kStages>;
   static bool attr = false;
@@ -440,7 +571,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, M, N, K, split, ep, cv);
+  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
@@ -475,14 +606,24 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   if (!make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, g->workspace};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, g->workspace, 0};
+  // staged TMA store whenever the output layout allows it (16-byte aligned rows)
+  CUtensorMap tcm;
+  memset(&tcm, 0, sizeof(tcm));
+  {
+    const int elem = g->out_f32 ? 4 : 2;
+    const int n_out = g->act == DRS_ACT_GEGLU ? N / 2 : N;
+    const bool ok = split == 1 && !(reinterpret_cast<uintptr_t>(g->C) & 15) && ((g->ldc * elem) % 16) == 0 &&
+                    g->ldc >= n_out;
+    if (ok && make_tmap_out(&tcm, g->C, M, n_out, g->ldc, elem, g->act == DRS_ACT_GEGLU ? 16 : 32)) ep.tma_store = 1;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, M, N, K, split, ep, cv, st);
-  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, M, N, K, split, ep, cv, st);
-  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, M, N, K, split, ep, cv, st);
-  else if (bn == 192) rc = launch_gemm<192, 5>(ta, tb, M, N, K, split, ep, cv, st);
-  else rc = launch_gemm<256, 4>(ta, tb, M, N, K, split, ep, cv, st);
+  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  else if (bn == 192) rc = launch_gemm<192, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  else rc = launch_gemm<256, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
   if (rc != DRS_OK || split == 1) return rc;
   const int64_t threads = (int64_t)M * ((N + 31) / 32);
   launch_pdl(gemm_reduce_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, M, N, split, ep);

@@ -26,8 +26,9 @@ extern "C" {
  * A, B bf16 K-major (lda/ldb in elements, multiples of 8, 16-byte aligned),
  * C bf16 (out_f32 = 0) or fp32, residual bf16 or NULL, bias fp32 or NULL.
  * tcgen05.mma (M=128, N=bn in {64,128,256}) with TMA-fed SWIZZLE_128B smem
- * ring and a double-buffered TMEM accumulator; split > 1 = deterministic
- * split-K through `workspace` (split*M*N fp32). */
+ * ring and a double-buffered TMEM accumulator; split in 2..8 = deterministic
+ * split-K over a thread-block cluster (partials reduced through DSMEM in a
+ * fixed order); `workspace` is unused (kept for ABI stability, may be NULL). */
 int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int M, int N, int K, const float* bias, const void* residual, int64_t ldr,
                   int act, int out_f32, float alpha, int bn, int split, float* workspace, void* stream);
@@ -56,6 +57,14 @@ typedef struct drs_gemm_args {
   int conv_N, conv_H, conv_W, conv_C;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
+
+/* Tile width / split-K the library picks when drs_gemm gets bn == 0 and/or
+ * split == 0 (in/out: nonzero inputs are kept).  Cost model calibrated on
+ * B200 (per-SM operand streaming rate, MMA rate, launch and cluster-reduce
+ * latency, cluster co-residency from cudaOccupancyMaxActiveClusters). */
+int drs_gemm_pick(int M, int N, int K, int* bn, int* split);
+/* The model's time for one configuration, in ns (-1 on bad arguments). */
+int drs_gemm_cost_us(int M, int N, int K, int bn, int split);
 
 /* out[m, :] = LN(x[m, :]) (*gamma + beta) (*(1 + scale) + shift) -> bf16.
  * x fp32 (x_f32 = 1) or bf16; gamma/beta fp32 [C] or NULL; shift/scale fp32

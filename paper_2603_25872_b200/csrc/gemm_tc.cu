@@ -14,9 +14,11 @@
 //                 32-column chunks: tcgen05.ld 32x32b -> registers -> bias /
 //                 GELU / SiLU / GEGLU / gate / residual -> bf16 or fp32 stores
 // Grid = min(#tiles, #SMs); each CTA walks tiles t = blockIdx.x, +gridDim.x.
-// Split-K (kSplit > 1): each split accumulates a K range and writes fp32
-// partials; drs_gemm_reduce sums them in a fixed order (deterministic, no
-// atomics) and applies the same epilogue.
+// Split-K (split > 1): the `split` CTAs of one output tile form a thread-block
+// cluster; each accumulates a K range, parks its fp32 partial tile in its own
+// (idle) pipeline shared memory, and after a cluster barrier every CTA reduces
+// a slice of the tile's rows over DSMEM in the fixed order s = 0..split-1
+// (deterministic, no atomics, no workspace) and runs the common epilogue.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -56,7 +58,6 @@ struct EpiParams {
   float alpha;
   int act;                  // DRS_ACT_*
   int out_f32;              // 1: fp32 output, 0: bf16
-  float* partial;           // split-K workspace [split][M][N] fp32 (split > 1)
   int tma_store;            // 1: output written through smem staging + TMA (tmap_c)
 };
 
@@ -244,6 +245,21 @@ __device__ __forceinline__ void stage_rows(uint8_t* buf, int lane, int pitch, bo
   }
 }
 
+// thread-block cluster helpers (split-K reduction)
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t smem_addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 dsmem_ld4(uint32_t addr) {
+  float4 f;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w) : "r"(addr) : "memory");
+  return f;
+}
 __device__ __forceinline__ void fence_async_smem_g() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
@@ -421,11 +437,11 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = kb1 > kb0 ? __uint_as_float(r[j]) : 0.f;
         if (split > 1) {
-          if (row < M) {
-            float* dst = ep.partial + ((int64_t)sp * M + row) * N + n0;
+          // partial tile -> this CTA's smem (padded rows: conflict-free float4 stores)
+          float* dst = reinterpret_cast<float*>(smem) + (quad * 32 + lane) * (BN + 4) + c * 32;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = v[j];
-          }
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else if (ep.tma_store) {
           epi_math32(ep, M, N, row, n0, v);
           // the buffer about to be written must have been read by its last store
@@ -452,38 +468,45 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     }
     if (ep.tma_store && lane == 0) bulk_wait_all();
   }
+  if (split > 1) {
+    // ---------------- cluster split-K reduction over DSMEM ----------------
+    // (non-persistent: this CTA computed exactly one (tile, split) unit; its
+    // cluster rank is its split index)
+    __syncwarp();
+    cluster_sync();                                // every partial tile is in smem
+    if (warp >= 2) {
+      const int sp = blockIdx.x % split;
+      const int mn = blockIdx.x / split;
+      const int mt = mn % m_tiles, nt = mn / m_tiles;
+      const int t = threadIdx.x - 64;              // 0..255
+      const uint32_t base = tc::smem_u32(smem);
+      constexpr int kChunks = BN / 32;
+      const int rows_here = (kBM - sp + split - 1) / split;      // rows sp, sp+split, ...
+      for (int item = t; item < rows_here * kChunks; item += kEpiWarps * 32) {
+        const int r = sp + (item / kChunks) * split;
+        const int c = item % kChunks;
+        const int n0 = nt * BN + c * 32;
+        if (n0 >= N) continue;
+        const uint32_t off = (uint32_t)((r * (BN + 4) + c * 32) * 4);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        for (int s2 = 0; s2 < split; ++s2) {
+          const uint32_t ra = dsmem_map(base + off, s2);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 f = dsmem_ld4(ra + 16 * q);
+            v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+          }
+        }
+        epilogue32(ep, M, N, mt * kBM + r, n0, v);
+      }
+    }
+    __syncwarp();
+    cluster_sync();                                // peers are done reading this CTA's smem
+  }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem_base);
-}
-
-// Deterministic split-K reduction + epilogue.  A warp owns one row and 32
-// consecutive 32-column chunks: each lane sums its chunk's partials (fixed
-// split order) with float4 loads, then runs the common epilogue.
-__global__ void gemm_reduce_kernel(int M, int N, int split, EpiParams ep) {
-  pdl_wait();
-  pdl_trigger();
-  const int chunks = (N + 31) / 32;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;          // host: M * chunks < 2^31
-  if (idx >= M * chunks) return;
-  const int row = idx / chunks, n0 = (idx - row * chunks) * 32;
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = 0.f;
-  const bool full = n0 + 32 <= N && (N % 4) == 0;
-  for (int s = 0; s < split; ++s) {
-    const float* src = ep.partial + ((int64_t)s * M + row) * N + n0;
-    if (full) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(src) + q);
-        v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += src[j];
-    }
-  }
-  epilogue32(ep, M, N, row, n0, v);
 }
 
 // ------------------------------------------------------------ host side ---
@@ -559,23 +582,147 @@ static int num_sms() {
 }
 
 template <int BN, int kStages>
+static bool ensure_smem_attr() {
+  static int state = 0;        // 0 unknown, 1 ok, -1 failed
+  if (!state) {
+    using S = GemmSmem<BN, kStages>;
+    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 S::kBytes) == cudaSuccess ? 1 : -1;
+  }
+  return state > 0;
+}
+
+// Clusters of `split` CTAs of this configuration that fit on the GPU at once
+// (GPC packing makes this less than #SMs / split); cached per split.
+template <int BN, int kStages>
+static int max_clusters(int split) {
+  static int cache[9] = {0};
+  if (split < 2 || split > 8) return num_sms();
+  if (!cache[split]) {
+    using S = GemmSmem<BN, kStages>;
+    int n = 0;
+    if (ensure_smem_attr<BN, kStages>()) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(split * 64);
+      cfg.blockDim = dim3(kGemmThreads);
+      cfg.dynamicSmemBytes = S::kBytes;
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeClusterDimension;
+      la[0].val.clusterDim.x = split;
+      la[0].val.clusterDim.y = 1;
+      la[0].val.clusterDim.z = 1;
+      cfg.attrs = la;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages>, &cfg) != cudaSuccess) n = 0;
+      cudaGetLastError();
+    }
+    cache[split] = n > 0 ? n : num_sms() / split;
+  }
+  return cache[split];
+}
+
+template <int BN, int kStages>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, int M, int N, int K,
                        int split, const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
   auto kern = gemm_bf16_tc_kernel<BN, kStages>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
-      return DRS_ERR_CUDA;
-    attr = true;
-  }
+  if (!ensure_smem_attr<BN, kStages>()) return DRS_ERR_CUDA;
+  static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "split-K partial tile must fit the stage ring");
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
+  if (split == 1) {
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
+    return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+  }
+  // split-K: one CTA per (tile, split), the split CTAs of a tile as one cluster
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = S::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = split;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, M, N, K, split, ep, cv);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+static int max_clusters_bn(int bn, int split) {
+  switch (bn) {
+    case 64: return max_clusters<64, 8>(split);
+    case 128: return max_clusters<128, 6>(split);
+    case 160: return max_clusters<160, 5>(split);
+    case 192: return max_clusters<192, 4>(split);
+    default: return max_clusters<256, 4>(split);
+  }
+}
+
+// Modelled time (us) of one launch, calibrated on B200 with tools/gemm_sweep.py:
+//  * operand streaming: a CTA pulls its k-blocks at <= ~130 GB/s (L2 -> SM) and
+//    all CTAs together at <= ~11 TB/s (aggregate L2 -> SM); MMA at ~15.5
+//    TFLOP/s per SM; the slowest of the three bounds;
+//  * ~5 us fixed latency per launch (prologue, first loads, epilogue drain);
+//  * cluster split-K only when every cluster is co-resident (one wave: the
+//    split grid is not persistent) and costs ~1 us + 0.012 us * bn * (split-1)
+//    for the DSMEM partial-tile exchange.
+static double gemm_cost_us(int M, int N, int K, int bn, int split) {
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
+  const int kb = (K + kBK - 1) / kBK;
+  if (split > 1 && tiles > max_clusters_bn(bn, split)) return 1e30;
+  const int waves = split > 1 ? 1 : (tiles + num_sms() - 1) / num_sms();
+  const double kb_cta = (double)waves * ((kb + split - 1) / split);
+  const double kb_bytes = (double)(kBM + bn) * kBK * 2;
+  const double per_cta = kb_cta * kb_bytes / 130e3;
+  const double aggregate = (double)tiles * kb * kb_bytes / 11e6;
+  const double mma = kb_cta * 2.0 * kBM * bn * kBK / 15.5e6;
+  double t = per_cta > aggregate ? per_cta : aggregate;
+  if (mma > t) t = mma;
+  return 5.0 + t + (split > 1 ? 1.0 + 0.012 * bn * (split - 1) : 0.0);
+}
+
+// bn == 0: choose the tile width; split == 0: choose the split (<= 6).
+static void gemm_auto_config(int M, int N, int K, int& bn, int& split) {
+  static const int kBns[5] = {64, 128, 160, 192, 256};
+  static const int kSplits[5] = {1, 2, 3, 4, 6};
+  const int kb = (K + kBK - 1) / kBK;
+  double best = 1e30;
+  int bb = bn ? bn : 128, bs = split ? split : 1;
+  for (int i = 0; i < 5; ++i) {
+    if (bn && kBns[i] != bn) continue;
+    for (int j = 0; j < 5; ++j) {
+      if (split && kSplits[j] != split) continue;
+      if (kSplits[j] > 1 && kb / kSplits[j] < 8) continue;      // keep >= 8 k-blocks per split
+      const double t = gemm_cost_us(M, N, K, kBns[i], kSplits[j]);
+      if (t >= 1e29) continue;
+      if (t < best * 0.97) { best = t; bb = kBns[i]; bs = kSplits[j]; }   // ties -> smaller tile / split
+    }
+  }
+  bn = bb;
+  split = bs;
+}
+
 }  // namespace drs
+
+extern "C" int drs_gemm_cost_us(int M, int N, int K, int bn, int split) {
+  if (M <= 0 || N <= 0 || K <= 0 || split < 1 || split > 8) return -1;
+  const double t = drs::gemm_cost_us(M, N, K, bn, split);
+  return t >= 1e29 ? -1 : (int)(t * 1000.0);   // ns; -1 = configuration not allowed
+}
+
+extern "C" int drs_gemm_pick(int M, int N, int K, int* bn, int* split) {
+  if (!bn || !split || M <= 0 || N <= 0 || K <= 0) return DRS_ERR_VALUE;
+  int b = *bn, s = *split;
+  drs::gemm_auto_config(M, N, K, b, s);
+  *bn = b;
+  *split = s;
+  return DRS_OK;
+}
 
 extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   using namespace drs;
@@ -587,10 +734,10 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if ((reinterpret_cast<uintptr_t>(g->A) & 15) || (reinterpret_cast<uintptr_t>(g->B) & 15)) return DRS_ERR_VALUE;
   if (g->act == DRS_ACT_GEGLU && (N % 2)) return DRS_ERR_VALUE;
   if (g->rowbias && g->rb_group <= 0) return DRS_ERR_VALUE;
-  int bn = g->bn ? g->bn : 128;
-  if (bn != 64 && bn != 128 && bn != 160 && bn != 192 && bn != 256) return DRS_ERR_VALUE;
-  const int split = g->split < 1 ? 1 : g->split;
-  if (split > 1 && !g->workspace) return DRS_ERR_VALUE;
+  int bn = g->bn, split = g->split;
+  if (bn != 0 && bn != 64 && bn != 128 && bn != 160 && bn != 192 && bn != 256) return DRS_ERR_VALUE;
+  if (split < 0 || split > 8) return DRS_ERR_VALUE;            // portable cluster size
+  if (bn == 0 || split == 0) gemm_auto_config(M, N, K, bn, split);
   CUtensorMap ta, tb;
   ConvGeom cv{0, 0, 0, 0};
   if (g->conv_C > 0) {      // implicit 3x3 conv: A = NHWC input, M = N*H*W, K = 9*C
@@ -606,7 +753,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   if (!make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, g->workspace, 0};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   CUtensorMap tcm;
   memset(&tcm, 0, sizeof(tcm));
@@ -624,10 +771,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, tcm, M, N, K, split, ep, cv, st);
   else if (bn == 192) rc = launch_gemm<192, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
   else rc = launch_gemm<256, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  if (rc != DRS_OK || split == 1) return rc;
-  const int64_t threads = (int64_t)M * ((N + 31) / 32);
-  launch_pdl(gemm_reduce_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, st, M, N, split, ep);
-  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+  return rc;
 }
 
 extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,

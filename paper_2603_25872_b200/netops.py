@@ -5,25 +5,19 @@ raises if libdrs.so is missing (no fallback).  Weights are bf16, K-major
 (nn.Linear layout: W[out, in]); activations bf16; accumulation fp32.
 """
 
+import json
+import os
+
 import torch
 
 from . import _lib
 
 ACT = {None: 0, "none": 0, "gelu_tanh": 1, "silu": 2, "gelu": 3, "geglu": 4}
 
-_ws = {}
 
 # Instrumentation (bench.py): when TIMERS is a list, every GEMM records
 # (flops, start event, end event) on the current stream.
 TIMERS = None
-
-
-def _workspace(device, numel):
-    buf = _ws.get(device)
-    if buf is None or buf.numel() < numel:
-        buf = torch.empty(max(numel, 1 << 20), dtype=torch.float32, device=device)
-        _ws[device] = buf
-    return buf
 
 
 def _ptr(t):
@@ -65,15 +59,14 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     if rowbias is not None:
         assert rowbias.dtype == torch.float32 and rb_group > 0
         g.rowbias, g.rb_group, g.rb_ld = rowbias.data_ptr(), rb_group, rowbias.stride(0)
-    if bn == 0:
-        bn = pick_bn(M, N)
-    if split == 0:
-        split = pick_split(M, N, K, bn)
+    if SHAPES is not None:
+        SHAPES.append((M, N, K, act, residual is not None and residual.dtype == torch.float32,
+                       residual is not None, out.dtype == torch.float32, None if conv is None else tuple(conv)))
+    if bn == 0 or split == 0:                    # tuned table, else the library cost model
+        bn, split = pick(M, N, K, bn, split, conv is not None)
     g.bn, g.split = bn, split
     if conv is not None:
         g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
-    if split > 1:
-        g.workspace = _workspace(x.device, split * M * N).data_ptr()
     if TIMERS is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -87,19 +80,37 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
 BN_CHOICES = (64, 128, 160, 192, 256)
 
 
-def pick_bn(M, N, sms=148):
-    """Tile width maximising useful tile area per wave of SMs (UMMA N is any
-    multiple of 16, so 160/192 fit the UNet's 320/640/960 channel counts)."""
-    m_tiles = (M + 127) // 128
-    best, best_eff = 128, -1.0
-    for bn in BN_CHOICES:
-        tiles = m_tiles * ((N + bn - 1) // bn)
-        waves = (tiles + sms - 1) // sms
-        eff = (M * N) / (waves * sms * 128.0 * bn)
-        eff *= 1.0 + 0.15 * (bn / 256.0)          # larger tiles reuse the A tile more
-        if eff > best_eff:
-            best, best_eff = bn, eff
-    return best
+_TABLE_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gemm_table.json")
+_TABLE = None
+SHAPES = None      # when a list: linear() appends (M, N, K, act, res_f32, has_res, out_f32, conv) (tuning)
+
+
+def _table():
+    global _TABLE
+    if _TABLE is None:
+        try:
+            with open(_TABLE_PATH) as f:
+                _TABLE = {k: tuple(v) for k, v in json.load(f)["configs"].items()}
+        except (OSError, ValueError, KeyError):
+            _TABLE = {}
+    return _TABLE
+
+
+def table_key(M, N, K, conv=False):
+    return f"{M}x{N}x{K}" + (":conv" if conv else "")
+
+
+def pick(M, N, K, bn=0, split=0, conv=False):
+    """(bn, split) for this GEMM: explicit values win; otherwise the measured
+    B200 table (tools/gemm_tune.py -> gemm_table.json) for shapes the networks
+    issue, else the library's cost model (drs_gemm_pick)."""
+    if bn == 0 and split == 0:
+        hit = _table().get(table_key(M, N, K, conv))
+        if hit is not None:
+            return hit
+    b, sp = _lib.ctypes.c_int(bn), _lib.ctypes.c_int(split)
+    _lib.check(_lib.lib().drs_gemm_pick(M, N, K, _lib.ctypes.byref(b), _lib.ctypes.byref(sp)), "drs_gemm_pick")
+    return b.value, sp.value
 
 
 def implicit_conv_ok(N, H, W, C):
@@ -112,16 +123,6 @@ def implicit_conv_ok(N, H, W, C):
     if W * rows * imgs != 128 or H % rows:
         return False
     return imgs == 1 or (rows == H and N % imgs == 0)
-
-
-def pick_split(M, N, K, bn):
-    """Deterministic split-K (fp32 partials + fixed-order reduce) when the tile
-    grid leaves most SMs idle AND each split still has a long K loop."""
-    tiles = ((M + 127) // 128) * ((N + bn - 1) // bn)
-    kb = (K + 63) // 64
-    if tiles > 74 or kb < 48:
-        return 1
-    return max(1, min(kb // 16, 148 // tiles, 8))
 
 
 def layernorm(x, out=None, gamma=None, beta=None, shift=None, scale=None, eps=1e-6, mod_group=0):

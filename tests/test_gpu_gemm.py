@@ -70,3 +70,52 @@ def test_implicit_conv3x3(cuda, N, H, W, C, Co):
     ref = ref.permute(0, 2, 3, 1).reshape(N * H * W, Co)
     rel = ((y - ref).norm() / ref.norm()).item()
     assert rel < 5e-3, rel
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 1280, 11520), (300, 200, 1152), (77, 768, 320), (256, 1152, 128)])
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("split", [2, 3, 5, 8])
+def test_gemm_cluster_splitk(cuda, M, N, K, bn, split):
+    """Cluster split-K (DSMEM reduction): vs fp32 torch, bit-identical across runs
+    (fixed reduction order); K=128 with split >= 3 leaves some splits empty."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    r = torch.randn(M, N, device=cuda, generator=g).bfloat16()
+    y1 = linear(x, w, bias=b, residual=r, out_dtype=torch.float32, bn=bn, split=split)
+    y2 = linear(x, w, bias=b, residual=r, out_dtype=torch.float32, bn=bn, split=split)
+    ref = _ref(x, w, b, None, r, 1.0)
+    err = (y1 - ref).abs().max().item()
+    assert err <= 2e-3 * max(1.0, ref.abs().max().item()), (M, N, K, bn, split, err)
+    assert torch.equal(y1, y2)
+
+
+def test_gemm_auto_pick(cuda):
+    """Library-chosen (bn, split) are valid and the default path matches torch."""
+    from paper_2603_25872_b200.netops import linear, pick
+    for (M, N, K) in [(128, 1280, 11520), (512, 1280, 1280), (8192, 320, 2880), (256, 1152, 4608)]:
+        bn, split = pick(M, N, K)
+        assert bn in (64, 128, 160, 192, 256) and 1 <= split <= 8
+        assert pick(M, N, K, bn=64)[0] == 64 and pick(M, N, K, split=2)[1] == 2
+        g = torch.Generator(device=cuda).manual_seed(M)
+        x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+        w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+        y = linear(x, w, out_dtype=torch.float32)
+        ref = _ref(x, w, None, None, None, 1.0)
+        assert (y - ref).abs().max().item() <= 2e-3 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("split", [2, 4])
+def test_implicit_conv3x3_splitk(cuda, split):
+    from paper_2603_25872_b200.netops import linear
+    N, H, W, C, Co = 2, 8, 8, 1280, 1280
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x = torch.randn(N, H, W, C, device=cuda, generator=g).bfloat16()
+    wt = (torch.randn(Co, 3, 3, C, device=cuda, generator=g) * 0.02).bfloat16()
+    y = linear(x.reshape(-1, C), wt.reshape(Co, -1), out_dtype=torch.float32, conv=(N, H, W, C), split=split)
+    ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), wt.permute(0, 3, 1, 2).float(), padding=1)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Co)
+    err = (y - ref).abs().max().item()
+    assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err

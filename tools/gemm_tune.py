@@ -1,0 +1,139 @@
+"""Measure the best (bn, split) for every GEMM shape the denoiser networks
+issue and write paper_2603_25872_b200/gemm_table.json (read by netops.pick).
+
+Each candidate is timed inside a CUDA graph of back-to-back launches with the
+shape's own epilogue (activation, residual dtype, output dtype, implicit conv),
+which is how the network graphs run it.  The table is keyed by M x N x K
+(+ ":conv"), so the result is deterministic for a given table.
+
+    python tools/gemm_tune.py [--nets sd15:1,2,4,8 dit:1,2,4,8 sdxl:1,2] [--out PATH]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+BNS = (64, 128, 160, 192, 256)
+SPLITS = (1, 2, 3, 4, 6, 8)
+
+
+def collect(net_name, batches, dev):
+    import torch
+    from paper_2603_25872_b200 import netops
+    bmax = max(batches)
+    if net_name == "dit":
+        from paper_2603_25872_b200.dit import DiT, DiTConfig
+        net, D = DiT(DiTConfig(), dev, max_batch=bmax), 4 * 32 * 32
+    else:
+        from paper_2603_25872_b200.unet import UNet, sd15_config, sdxl_config
+        net = UNet(sd15_config() if net_name == "sd15" else sdxl_config(), dev, max_batch=bmax)
+        D = net.latent_numel
+    shapes = []
+    for B in batches:
+        xs = [torch.randn(D, device=dev, dtype=torch.float64) for _ in range(B)]
+        outs = [torch.empty(D, device=dev) for _ in range(B)]
+        netops.SHAPES = []
+        net.forward(xs, torch.full((B,), 500.0, device=dev), B, outs)
+        torch.cuda.synchronize()
+        shapes += netops.SHAPES
+        netops.SHAPES = None
+    del net
+    torch.cuda.empty_cache()
+    return shapes
+
+
+def time_config(run, reps):
+    import torch
+    run()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            run()
+    g.replay()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e3 / reps)
+    return best
+
+
+def tune_shape(desc, dev, reps):
+    import torch
+    from paper_2603_25872_b200.netops import linear, pick
+    M, N, K, act, res_f32, has_res, out_f32, conv = desc
+    if conv is not None:
+        cn, ch, cw, cc = conv
+        x = torch.randn(cn * ch * cw, cc, device=dev).bfloat16()
+    else:
+        x = torch.randn(M, K, device=dev).bfloat16()
+    w = (torch.randn(N, K, device=dev) * 0.02).bfloat16()
+    n_out = N // 2 if act == "geglu" else N
+    out = torch.empty(M, n_out, device=dev, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    res = None
+    if has_res:
+        res = torch.randn(M, n_out, device=dev, dtype=torch.float32 if res_f32 else torch.bfloat16)
+    bias = torch.randn(N, device=dev)
+    tiles_of = lambda bn: ((M + 127) // 128) * ((N + bn - 1) // bn)   # noqa: E731
+    kb = (K + 63) // 64
+    results = {}
+    for bn in BNS:
+        for sp in SPLITS:
+            if sp > 1 and (tiles_of(bn) * sp > 148 or kb // sp < 4):
+                continue
+            run = lambda bn=bn, sp=sp: linear(x, w, bias=bias, act=act, residual=res, out=out,   # noqa: E731
+                                              bn=bn, split=sp, conv=conv)
+            results[(bn, sp)] = time_config(run, reps)
+    best = min(results, key=results.get)
+    model = pick(M, N, K, 0, 0, False) if conv is None else None
+    return best, results[best], results, model
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nets", nargs="+", default=["sd15:1,2,4,8", "dit:1,2,4,8", "sdxl:1,2"])
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--out", default=os.path.join(ROOT, "paper_2603_25872_b200", "gemm_table.json"))
+    a = ap.parse_args()
+    import torch
+    from paper_2603_25872_b200 import netops
+    netops._TABLE = {}                       # tune against the model, not an old table
+    dev = torch.device("cuda", 0)
+    uniq = {}
+    for spec in a.nets:
+        name, bs = spec.split(":")
+        for d in collect(name, [int(b) for b in bs.split(",")], dev):
+            key = netops.table_key(d[0], d[1], d[2], d[7] is not None)
+            uniq.setdefault(key, d)
+    print(f"{len(uniq)} unique GEMM shapes", flush=True)
+    table, t0 = {}, time.time()
+    tot_best = tot_model = 0.0
+    for key, d in sorted(uniq.items()):
+        best, us, res, model = tune_shape(d, dev, a.reps)
+        table[key] = list(best)
+        mt = res.get(model, float("nan")) if model else float("nan")
+        if model in res:
+            tot_best += us
+            tot_model += mt
+        print(f"{key:24s} best bn={best[0]:3d} split={best[1]} {us:8.1f} us   model {model} {mt:8.1f} us",
+              flush=True)
+    print(f"tuned {len(table)} shapes in {time.time() - t0:.0f} s; sum best {tot_best:.0f} us vs model "
+          f"{tot_model:.0f} us (shapes the model covers)")
+    with open(a.out, "w") as f:
+        json.dump({"device": torch.cuda.get_device_name(0), "tool": "tools/gemm_tune.py",
+                   "configs": dict(sorted(table.items()))}, f, indent=1)
+        f.write("\n")
+    print("wrote", a.out)
+
+
+if __name__ == "__main__":
+    main()

@@ -100,10 +100,15 @@ int drs_cast_f32_bf16(const float* x, int64_t n, void* out_bf16, void* stream);
  * stride/pad, nearest-upsampled input when up = 2.  C1, C2 multiples of 8. */
 int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N, int H, int W, int ks, int stride,
                int pad, int up, void* out, void* stream);
-/* GroupNorm(G) + affine (+ SiLU) over NHWC: parallel partial sums (no atomics,
- * bit-reproducible) + fused finalize/apply.  workspace: N*G*16 float2. HW % 16 == 0. */
+/* GroupNorm(G) + affine (+ SiLU) over NHWC -> bf16, bit-reproducible (fixed
+ * reduction order, no atomics).  C % 8 == 0, C/G >= 8, G <= 32, input
+ * <= 12 MB, 16-byte aligned x/out: one launch of thread-block clusters (per image x group chunk;
+ * partial sums exchanged over DSMEM, input slice kept in shared memory);
+ * workspace unused (may be NULL).  Otherwise two kernels (HW % 16 == 0) with
+ * drs_groupnorm_workspace_bytes(N, G) bytes of workspace. */
 int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma, const float* beta,
                   float eps, int silu, void* out, void* workspace, void* stream);
+size_t drs_groupnorm_workspace_bytes(int N, int G);
 int drs_latent_to_nhwc(const void* x, int x_f64, int C, int HW, int Cpad, void* out, void* stream);
 /* eps (C,H,W) fp32 = u + g (c - u) from NHWC fp32 rows [uncond | cond] (pair = 1) */
 int drs_cfg_combine(const float* y, int64_t ld, int HW, int C, float g, int pair, float* eps, void* stream);

@@ -35,12 +35,18 @@ constexpr int kBK = 64;                 // one 128-byte swizzle atom of bf16
 constexpr int kGemmThreads = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM quadrant)
 constexpr int kEpiWarps = 8;
 
+// tanh on the SFU (tanh.approx.f32, rel. error ~2^-11: below the bf16 rounding of the output)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.7071067811865476f)); }
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
 
 struct EpiParams {
   void* out;

@@ -13,6 +13,10 @@
 
 namespace drs {
 
+// x * sigmoid(x) with the fast reciprocal (an IEEE division costs ~10x more;
+// __fdividef(1, inf) = 0 gives the right limit for very negative x)
+__device__ __forceinline__ float silu_fast(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
+
 // ------------------------------------------------------------ LayerNorm ---
 // One warp per row, float4-vectorised; x and the modulation vectors are all
 // loaded before any arithmetic so the warp pays one memory round trip.
@@ -419,7 +423,11 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     float a = 0.f, b = 0.f;
     const float2* pp = part + ((int64_t)n * G + g) * kGnSplit;
-    for (int s2 = 0; s2 < kGnSplit; ++s2) { a += pp[s2].x; b += pp[s2].y; }
+    float2 f[kGnSplit];
+#pragma unroll
+    for (int s2 = 0; s2 < kGnSplit; ++s2) f[s2] = pp[s2];
+#pragma unroll
+    for (int s2 = 0; s2 < kGnSplit; ++s2) { a += f[s2].x; b += f[s2].y; }
     const float cnt = (float)HW * cg;
     const float mean = a / cnt;
     const float var = fmaxf(b / cnt - mean * mean, 0.f);
@@ -444,10 +452,240 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
 #pragma unroll
     for (int pp = 0; pp < kGnPix; ++pp) {
       float v0 = v[pp].x * a0 + b0, v1 = v[pp].y * a1 + b1;
-      if (silu) { v0 = v0 / (1.f + __expf(-v0)); v1 = v1 / (1.f + __expf(-v1)); }
+      if (silu) { v0 = silu_fast(v0); v1 = silu_fast(v1); }
       *reinterpret_cast<__nv_bfloat162*>(out + (pix0 + pp) * C + c) = __floats2bfloat162_rn(v0, v1);
     }
   }
+}
+
+// ---- fused GroupNorm: one launch, one pass over HBM, cluster reduction ----
+// A thread-block cluster of kGnCs CTAs owns one (image, chunk of gpc groups);
+// its CTAs split the image's pixels.  Each CTA streams its rows x (cg * gpc)
+// channels with 16-byte loads (thread = one 8-channel pack; a pack spans at
+// most two groups since C/G >= 8), keeps the slice in shared memory when it
+// fits, and reduces per-group (sum, sumsq) in a fixed order.  After one
+// hardware cluster barrier every CTA sums the kGnCs partials of its groups
+// over DSMEM in rank order (bit-reproducible, no atomics, no workspace) and
+// applies (x - mean) * rstd * gamma + beta (+ SiLU) from shared memory.
+constexpr int kGnCs = 8;                      // CTAs per cluster (portable size)
+
+__device__ __forceinline__ void gn_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float2 gn_dsmem_ld2(const void* local, int rank) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float2 f;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(f.x), "=f"(f.y) : "r"(r) : "memory");
+  return f;
+}
+
+template <bool F32>
+__device__ __forceinline__ void gn_load8(const void* base, int64_t idx, float (&v)[8]) {
+  if (F32) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + idx));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + idx) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + idx));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(h[e]); v[2 * e] = f.x; v[2 * e + 1] = f.y; }
+  }
+}
+
+#ifdef DRS_GN_TIMING
+__device__ unsigned long long g_gn_ts[5][2048];
+__device__ __forceinline__ void gn_stamp(int i) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gn_ts[i][blockIdx.x] = t;
+  }
+}
+#else
+__device__ __forceinline__ void gn_stamp(int) {}
+#endif
+
+template <bool F32>
+__global__ void __launch_bounds__(512)
+gn_cluster_kernel(const void* __restrict__ x, int HW, int C, int G, int gpc, const float* __restrict__ gamma,
+                  const float* __restrict__ beta, float eps, int silu, __nv_bfloat16* __restrict__ out, int rpc,
+                  int keep) {
+  extern __shared__ __align__(16) uint8_t gsm[];
+  constexpr int kElem = F32 ? 4 : 2;
+  const int cg = C / G, Cc = cg * gpc;                  // channels this cluster owns
+  const int P = Cc / 8, R = blockDim.x / P;              // packs per row, rows per sweep
+  const int t = threadIdx.x, q = t % P, rr = t / P;
+  const int rank = blockIdx.x % kGnCs, cl = blockIdx.x / kGnCs;
+  const int n_chunks = G / gpc;
+  const int n = cl / n_chunks, chunk = cl % n_chunks;
+  const int row0 = rank * rpc, row1 = min(HW, row0 + rpc);
+  const int cbase = chunk * Cc, c0 = 8 * q;             // c0: channel within the chunk
+  const int g_lo = c0 / cg, n_lo = min(8, (g_lo + 1) * cg - c0);
+  float4* red = reinterpret_cast<float4*>(gsm);          // [blockDim] (s_lo, ss_lo, s_hi, ss_hi)
+  float2* csum = reinterpret_cast<float2*>(gsm + blockDim.x * 16);   // [gpc] this CTA's partials
+  float* stat = reinterpret_cast<float*>(gsm + blockDim.x * 16 + 32 * 8);  // [gpc][2]
+  uint8_t* slice = gsm + blockDim.x * 16 + 32 * 8 + 32 * 8;         // [rpc][Cc]
+  const int64_t img = (int64_t)n * HW * C + cbase;
+  pdl_wait();
+  gn_stamp(0);
+  float s_lo = 0.f, ss_lo = 0.f, s_hi = 0.f, ss_hi = 0.f;
+  constexpr int kB = 4;                                  // rows in flight per thread
+  if (rr < R) {
+    for (int rb = row0 + rr; rb < row1; rb += kB * R) {
+      float v[kB][8];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int r = rb + i * R;
+        if (r < row1) gn_load8<F32>(x, img + (int64_t)r * C + c0, v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int r = rb + i * R;
+        if (r >= row1) break;
+        if (keep) {
+          uint8_t* d = slice + ((size_t)(r - row0) * Cc + c0) * kElem;
+          if (F32) {
+            reinterpret_cast<float4*>(d)[0] = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+            reinterpret_cast<float4*>(d)[1] = make_float4(v[i][4], v[i][5], v[i][6], v[i][7]);
+          } else {
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[i][2 * e], v[i][2 * e + 1]);   // exact
+            *reinterpret_cast<uint4*>(d) = u;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < n_lo) { s_lo += v[i][e]; ss_lo += v[i][e] * v[i][e]; }
+          else { s_hi += v[i][e]; ss_hi += v[i][e] * v[i][e]; }
+        }
+      }
+    }
+  }
+  red[t] = make_float4(s_lo, ss_lo, s_hi, ss_hi);
+  __syncthreads();
+  for (int g = t; g < gpc; g += blockDim.x) {            // fixed order: packs, then row lanes
+    float a = 0.f, b = 0.f;
+    const int qa = (g * cg) / 8, qb = ((g + 1) * cg - 1) / 8;
+    for (int qq = qa; qq <= qb; ++qq) {
+      const bool lo = (8 * qq) / cg == g;
+      for (int r2 = 0; r2 < R; ++r2) {
+        const float4 f = red[r2 * P + qq];
+        a += lo ? f.x : f.z;
+        b += lo ? f.y : f.w;
+      }
+    }
+    csum[g] = make_float2(a, b);
+  }
+  gn_stamp(1);
+  gn_cluster_sync();                                     // every CTA's partials are published
+  gn_stamp(2);
+  pdl_trigger();
+  for (int g = t; g < gpc; g += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int r2 = 0; r2 < kGnCs; ++r2) {                 // rank order: deterministic
+      const float2 f = gn_dsmem_ld2(&csum[g], r2);
+      a += f.x;
+      b += f.y;
+    }
+    const float cnt = (float)HW * cg;
+    const float mean = a / cnt;
+    const float var = fmaxf(b / cnt - mean * mean, 0.f);
+    stat[2 * g] = mean;
+    stat[2 * g + 1] = rsqrtf(var + eps);
+  }
+  gn_cluster_sync();                                     // stats read; peers may exit afterwards
+  gn_stamp(3);
+  if (rr >= R) return;
+  float sa[8], sb[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int g = (c0 + e) / cg;
+    sa[e] = stat[2 * g + 1] * __ldg(gamma + cbase + c0 + e);
+    sb[e] = __ldg(beta + cbase + c0 + e) - stat[2 * g] * sa[e];
+  }
+  for (int rb = row0 + rr; rb < row1; rb += kB * R) {
+    float v[kB][8];
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int r = rb + i * R;
+      if (r >= row1) break;
+      if (keep) {
+        const uint8_t* d = slice + ((size_t)(r - row0) * Cc + c0) * kElem;
+        if (F32) {
+          const float4 a4 = reinterpret_cast<const float4*>(d)[0], b4 = reinterpret_cast<const float4*>(d)[1];
+          v[i][0] = a4.x; v[i][1] = a4.y; v[i][2] = a4.z; v[i][3] = a4.w;
+          v[i][4] = b4.x; v[i][5] = b4.y; v[i][6] = b4.z; v[i][7] = b4.w;
+        } else {
+          const uint4 u = *reinterpret_cast<const uint4*>(d);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            v[i][2 * e] = f.x;
+            v[i][2 * e + 1] = f.y;
+          }
+        }
+      } else {
+        gn_load8<F32>(x, img + (int64_t)r * C + c0, v[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const int r = rb + i * R;
+      if (r >= row1) break;
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float y0 = v[i][2 * e] * sa[2 * e] + sb[2 * e], y1 = v[i][2 * e + 1] * sa[2 * e + 1] + sb[2 * e + 1];
+        if (silu) { y0 = silu_fast(y0); y1 = silu_fast(y1); }
+        h[e] = __floats2bfloat162_rn(y0, y1);
+      }
+      *reinterpret_cast<uint4*>(out + img + (int64_t)r * C + c0) = u;
+    }
+  }
+  gn_stamp(4);
+}
+
+static int gn_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// geometry of the cluster path (false: use the two-kernel path).  gpc = groups
+// per cluster: the smallest divisor of G whose channel span is a multiple of
+// 8 and that still leaves >= ~#SMs CTAs, so small batches fill the GPU.
+static bool gn_cluster_plan(int N, int HW, int C, int G, int x_f32, int& gpc, int& rpc, int& threads, int& keep,
+                            size_t& smem) {
+  const int cg = C / G;
+  if (C % 8 || cg < 8 || G > 32) return false;
+  // measured (tools/gn_bench.py): the cluster path wins up to ~12 MB of input;
+  // beyond that the two-kernel path's wider grid streams faster
+  if ((int64_t)N * HW * C * (x_f32 ? 4 : 2) > 12 * 1024 * 1024) return false;
+  gpc = 0;
+  for (int d = 1; d <= G; ++d) {
+    if (G % d || (cg * d) % 8 || (cg * d) / 8 > 512) continue;
+    if (!gpc) gpc = d;                                   // smallest legal chunk
+    if ((int64_t)N * (G / d) * kGnCs <= 2 * gn_num_sms()) { gpc = d; break; }
+  }
+  if (!gpc) return false;
+  const int P = cg * gpc / 8;
+  threads = P * (P >= 256 ? 1 : 256 / P);        // <= ~256 threads: two or more CTAs per SM
+  rpc = (HW + kGnCs - 1) / kGnCs;
+  const size_t base = (size_t)threads * 16 + 32 * 8 + 32 * 8;
+  const size_t slice = (size_t)rpc * cg * gpc * (x_f32 ? 4 : 2);
+  keep = base + slice <= 200 * 1024;
+  smem = base + (keep ? slice : 0);
+  return true;
 }
 
 // latent (C, H, W) fp64/fp32 -> NHWC bf16 with Cpad channels (zeros beyond C)
@@ -573,15 +811,50 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+extern "C" size_t drs_groupnorm_workspace_bytes(int N, int G) {
+  return (size_t)(N > 0 ? N : 0) * (G > 0 ? G : 0) * drs::kGnSplit * sizeof(float2);   // two-kernel path only
+}
+
 extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma,
                              const float* beta, float eps, int silu, void* out, void* workspace, void* stream) {
-  if (N <= 0 || HW <= 0 || G <= 0 || C % G || (C / G) % 2 || HW % kGnPix || !gamma || !beta || !workspace)
-    return DRS_ERR_VALUE;
+  using namespace drs;
+  if (N <= 0 || HW <= 0 || G <= 0 || C % G || (C / G) % 2 || !gamma || !beta) return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
+  int gpc, rpc, threads, keep;
+  size_t smem;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+      gn_cluster_plan(N, HW, C, G, x_f32, gpc, rpc, threads, keep, smem)) {
+    auto kern = x_f32 ? gn_cluster_kernel<true> : gn_cluster_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[x_f32 ? 1 : 0]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+        return DRS_ERR_CUDA;
+      attr[x_f32 ? 1 : 0] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(N * (G / gpc) * kGnCs);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute la[2];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = kGnCs;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, kern, x, HW, C, G, gpc, gamma, beta, eps, silu, static_cast<__nv_bfloat16*>(out), rpc,
+                       keep);
+    return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+  }
+  if (!workspace) return DRS_ERR_VALUE;
+  if (HW % kGnPix) return DRS_ERR_VALUE;
   float2* part = static_cast<float2*>(workspace);    // N*G*kGnSplit float2
   launch_pdl(gn_stats_kernel, dim3(dim3(N * G, kGnSplit)), dim3(256), 0, st, x, x_f32, HW, C, G, part);
   const int c2 = C / 2, thr = c2 >= 256 ? 256 : ((c2 + 31) / 32) * 32;
-  launch_pdl(gn_apply_kernel, dim3((unsigned)((int64_t)N * HW / kGnPix)), dim3(thr), 2 * G * sizeof(float), st, 
+  launch_pdl(gn_apply_kernel, dim3((unsigned)((int64_t)N * HW / kGnPix)), dim3(thr), 2 * G * sizeof(float), st,
       x, x_f32, HW, C, G, part, gamma, beta, eps, silu, static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -17,7 +17,7 @@ namespace drs {
 
 // runtime switch (drs_set_pdl): 1 = launch with the PDL attribute, 0 = plain stream order
 inline int& pdl_enabled() {
-  static int on = 0;   // measured: +1.5% on the SD1.5 UNet, -16% on batch-1 DiT -> off by default
+  static int on = 1;   // measured (net_bench, graph replay): SD1.5 -3%, DiT B=1 -3%, SDXL -1.2% time
   return on;
 }
 

@@ -191,6 +191,7 @@ def im2col(x1, C1, x2, C2, N, H, W, ks, stride, pad, up, out):
 
 
 _gn_ws = {}
+_gn_old = []
 
 # Instrumentation (bench.py): when TIMERS is a list, every GEMM records
 # (flops, start event, end event) on the current stream.
@@ -198,10 +199,14 @@ TIMERS = None
 
 
 def groupnorm(x, N, HW, C, G, gamma, beta, out, eps=1e-5, silu=False):
-    key = (x.device, N * G)
+    # workspace for the two-kernel fallback path only (the cluster path needs none)
+    key = x.device
+    need = int(_lib.lib().drs_groupnorm_workspace_bytes(N, G))
     ws = _gn_ws.get(key)
-    if ws is None:
-        ws = torch.empty(N * G * 16 * 2, dtype=torch.float32, device=x.device)
+    if ws is None or ws.numel() < need:
+        if ws is not None:
+            _gn_old.append(ws)               # may still be referenced by captured graphs
+        ws = torch.empty(max(need, 1 << 17), dtype=torch.uint8, device=x.device)
         _gn_ws[key] = ws
     _lib.check(_lib.lib().drs_groupnorm(x.data_ptr(), 1 if x.dtype == torch.float32 else 0, N, HW, C, G,
                                         gamma.data_ptr(), beta.data_ptr(), float(eps), 1 if silu else 0,

@@ -19,7 +19,7 @@ def test_header_symbols_exported(libdrs):
     decls = set()
     for h in ("drs.h", "drs_net.h"):
         hdr = open(os.path.join(ROOT, "include", h)).read()
-        decls |= set(re.findall(r"^(?:int|double)\s+(drs_\w+)\s*\(", hdr, re.M))
+        decls |= set(re.findall(r"^(?:int|double|size_t)\s+(drs_\w+)\s*\(", hdr, re.M))
     assert decls, "no declarations parsed"
     from paper_2603_25872_b200 import _lib
     assert decls == set(_lib.EXPORTED)

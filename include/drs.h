@@ -112,6 +112,16 @@ int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows, int64_t D
                const double* alpha_bar, int T, const double* means, const double* log_w,
                const double* var, int n_comp, double* const* out, int* err, void* stream);
 
+/* Euler family (next-row scope): VE-mixture ODE velocity (denoiser.py:124-136,
+ * replaces velocity_oracle at parallel.py:343-344 / sequential.py:125) for
+ * rows r < n_rows: x = xs[r], sigma = sigmas[idx[r]] (idx DEVICE int32 in
+ * 0..N), s_i = v_i + sigma**2, gain_i = v_i / s_i,
+ *   x0_hat = sum_i resp_i(x) (m_i + gain_i (x - m_i)),  v[r] = (x - x0_hat) / sigma.
+ * *err |= 2 for an index outside 0..N, |= 4 for sigma <= 0 (NonPositiveSigma). */
+int drs_gm_velocity(const double* const* xs, const int32_t* idx, int n_rows, int64_t D,
+                    const double* sigmas, int N, const double* means, const double* log_w,
+                    const double* var, int n_comp, double* const* out, int* err, void* stream);
+
 /* Copy rows: out[r][0..D) = src[r][0..D) (DEVICE pointer arrays). */
 int drs_copy_rows(const double* const* src, double* const* out, int n_rows, int64_t D,
                   void* stream);

@@ -27,6 +27,7 @@ SRC_ANCHOR = 2
 OP_SAVE_ANCHOR = 1
 ERR_NOISE_WINDOW_BIT = 1
 ERR_GM_TIMESTEP_BIT = 2
+ERR_GM_SIGMA_BIT = 4             # drs_gm_velocity: sigma <= 0 (NonPositiveSigma)
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -89,6 +90,10 @@ _SIGS = {
                                       ctypes.c_void_p]),
     "drs_skip_chain": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]),
     "drs_gm_eps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p]),
+    "drs_gm_velocity": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p]),

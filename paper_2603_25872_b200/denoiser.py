@@ -216,11 +216,63 @@ def state_independent_eps(seed: int, t: int, dim: int, *, device=None):
     return out
 
 
+def gm_velocity_launch(gm: GaussianMixture, sigmas, N: int, xs, idx, outs, err, stream=None):
+    """Launch K9 in VE-velocity mode for row lists xs/outs (CUDA fp64, gm.dim)
+    at sigma-table indices idx (sigmas: CUDA fp64, N+1 entries)."""
+    import torch
+    dev = outs[0].device
+    means, logw, var = gm.device_params(dev)
+    xs_p = _ptr_array(xs, dev)
+    out_p = _ptr_array(outs, dev)
+    idx_d = torch.tensor([int(i) for i in idx], dtype=torch.int32, device=dev)
+    st = _lib.lib().drs_gm_velocity(xs_p.data_ptr(), idx_d.data_ptr(), len(xs), gm.dim, sigmas.data_ptr(), N,
+                                    means.data_ptr(), logw.data_ptr(), var.data_ptr(), len(gm.weights),
+                                    out_p.data_ptr(), err.data_ptr(), _lib.stream_ptr(stream))
+    _lib.check(st, "drs_gm_velocity")
+    return (xs_p, out_p, idx_d)
+
+
 def velocity_oracle(gm: GaussianMixture, x, sigma: float):
-    """VE-mixture ODE velocity (denoiser.py:124-136): Euler family, next-row scope."""
+    """ODE velocity (x - x0_hat)/sigma of the variance-exploding mixture
+    p_sigma = sum_i w_i N(m_i, (v_i + sigma^2) I) (denoiser.py:124-136), on device."""
+    import torch
+    from .rng import _check_err
+    from .transitions import _device_of, as_device
     if not sigma > 0.0:
         raise NonPositiveSigma(f"sigma must be > 0, got {sigma}")
-    raise NotImplementedError("velocity_oracle (Euler family) is not on the B200 hot path yet")
+    dev = _device_of(x)
+    xd = as_device(x, dev, torch.float64)
+    if xd.shape[-1] != gm.dim:
+        raise DimensionMismatch(f"state dim {xd.shape[-1]} != mixture dim {gm.dim}")
+    flat = xd.reshape(-1, gm.dim)
+    out = torch.empty_like(flat)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    table = torch.tensor([float(sigma)], dtype=torch.float64, device=dev)
+    keep = gm_velocity_launch(gm, table, 0, _rows(flat, gm.dim), [0] * flat.shape[0], _rows(out, gm.dim), err)
+    _check_err(err)
+    del keep
+    return out.reshape(xd.shape)
+
+
+@dataclass(frozen=True, eq=False)
+class EulerVelocity:
+    """Engine core of the Euler family: the velocity of `gm` on sigma grid `g`;
+    a program task at "t" (remaining grid intervals) evaluates at sigma_{N-t}."""
+    gm: GaussianMixture
+    grid: object
+
+
+_EULER_CORES: dict = {}
+
+
+def euler_velocity_core(gm: GaussianMixture, g) -> EulerVelocity:
+    """One EulerVelocity per (mixture, grid) so compiled runs are reused."""
+    key = (id(gm), id(g))
+    core = _EULER_CORES.get(key)
+    if core is None or core.gm is not gm or core.grid is not g:
+        core = EulerVelocity(gm, g)
+        _EULER_CORES[key] = core
+    return core
 
 
 def latency_of(d):

@@ -18,7 +18,7 @@ import math
 import torch
 
 from . import _lib
-from .denoiser import (AnalyticEps, Counting, Latency, NetworkEps, Perturbed, StateIndependent,
+from .denoiser import (AnalyticEps, Counting, EulerVelocity, Latency, NetworkEps, Perturbed, StateIndependent,
                        latency_of, state_independent_key)
 from .program import Chain, Eval, Gather, Noise, Program
 from .rng import _STREAM_SALT, _SEED_MASK48, GENERATORS, _KeyBuffer, entropy_key
@@ -82,8 +82,8 @@ class DeviceRun:
         self.core, self.eval_ms, self.counters = unwrap(d)
         self.overhead_ms = (latency_of(d).dispatch_overhead_ms if latency_of(d) else 0.0)
         core = self.core
-        if isinstance(core, (AnalyticEps, StateIndependent)):
-            dim = core.gm.dim if isinstance(core, AnalyticEps) else core.dim
+        if isinstance(core, (AnalyticEps, StateIndependent, EulerVelocity)):
+            dim = core.dim if isinstance(core, StateIndependent) else core.gm.dim
             if dim < 1 or self.D % dim:
                 from .errors import DimensionMismatch
                 raise DimensionMismatch(f"denoiser dim {dim} does not tile state size {self.D}")
@@ -203,7 +203,7 @@ class DeviceRun:
             low = payload[1]
             if low is None:
                 return 0
-            if low[0] == "gm":
+            if low[0] in ("gm", "gmv"):
                 return low[1]["n"] * self.dim * 8 * (2 + low[1]["n_comp"])
             if low[0] == "copy":
                 return low[1]["n"] * self.dim * 16
@@ -239,6 +239,15 @@ class DeviceRun:
                 ts=torch.tensor(ts, dtype=torch.int32, device=self.device),
                 n=len(xs), n_tasks=len(local), means=means, logw=logw, var=var, n_comp=len(core.gm.weights),
                 alpha=self.s.device_alpha_bar(self.device)))
+        if isinstance(core, EulerVelocity):      # task t = remaining intervals: sigma_{N - t}
+            means, logw, var = core.gm.device_params(self.device)
+            N = core.grid.N
+            return ("gmv", dict(
+                xs=torch.tensor([x.data_ptr() for x in xs], dtype=torch.int64, device=self.device),
+                outs=torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64, device=self.device),
+                idx=torch.tensor([N - t for t in ts], dtype=torch.int32, device=self.device),
+                n=len(xs), n_tasks=len(local), means=means, logw=logw, var=var, n_comp=len(core.gm.weights),
+                sigmas=core.grid.device_sigmas(self.device), N=N))
         if isinstance(core, StateIndependent):
             src = [self.noise[self.rows[("si", t, None)]] for t in ts]
             return ("copy", dict(
@@ -263,6 +272,12 @@ class DeviceRun:
                               a["logw"].data_ptr(), a["var"].data_ptr(), a["n_comp"],
                               a["outs"].data_ptr(), self.err.data_ptr(), stream)
             _lib.check(st, "drs_gm_eps")
+        elif kind == "gmv":
+            st = L.drs_gm_velocity(a["xs"].data_ptr(), a["idx"].data_ptr(), a["n"], self.dim,
+                                   a["sigmas"].data_ptr(), a["N"], a["means"].data_ptr(),
+                                   a["logw"].data_ptr(), a["var"].data_ptr(), a["n_comp"],
+                                   a["outs"].data_ptr(), self.err.data_ptr(), stream)
+            _lib.check(st, "drs_gm_velocity")
         elif kind == "copy":
             _lib.check(L.drs_copy_rows(a["src"].data_ptr(), a["outs"].data_ptr(), a["n"], self.dim, stream),
                        "drs_copy_rows")

@@ -125,9 +125,24 @@ def run_conservative(s, d, x_T, devices: int, rule: VarianceRule, stream: RngStr
                 False, update_family, comm)
 
 
-def run_parallel_euler(g, gm, x_init, devices: int, mode: Mode, *, workers=None):
-    """Euler-family scheduler (parallel.py:324-381): next-row scope."""
-    raise NotImplementedError("Euler family (run_parallel_euler) is the next scope row; not built yet")
+def run_parallel_euler(g, gm, x_init, devices: int, mode: Mode, *, workers=None, comm: Comm | None = None):
+    """Euler-family variant of the two schedulers on a sigma grid with the
+    analytic velocity oracle (parallel.py:324-381).  Deterministic; timesteps
+    count remaining grid intervals; velocity tasks at sigma = 0 are dropped.
+    Same device program machinery as run_aggressive / run_conservative
+    (drafts from the anchor, one batched or rank-sharded velocity round,
+    fused refine chain; with `comm`, rank r evaluates tasks i % world == r)."""
+    from .denoiser import euler_velocity_core
+    _check_workers(workers, None)
+    plan = plan_blocks(g.N, devices, mode)
+    world = comm.size if comm else 1
+    rank = comm.rank if comm else 0
+    dev = resolve_device(x_init)
+    core = euler_velocity_core(gm, g)
+    run = get_run(("par", mode, "euler", g.N, devices, world, rank),
+                  lambda: build_parallel(g, plan, None, "euler", False, world, rank),
+                  g, core, _numel(x_init), dev, "pcg64", comm)
+    return execute(run, x_init, 0, None)
 
 
 __all__ = ["BlockPlan", "Comm", "Mode", "RoundReport", "Trajectory", "WORKER_CAP_ENV", "execute_round",

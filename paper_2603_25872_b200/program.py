@@ -27,7 +27,7 @@ from enum import Enum
 from . import _lib
 from .errors import InvalidPlanParams, InvalidSubsequence, PlanMismatch
 from .rng import Role
-from .transitions import VarianceRule, ddim_op_coeffs, ddpm_op_coeffs
+from .transitions import VarianceRule, ddim_op_coeffs, ddpm_op_coeffs, euler_op_coeffs
 
 
 class Mode(Enum):
@@ -141,7 +141,7 @@ class Program:
 class _Builder:
     def __init__(self, s, rule, family, world):
         self.s, self.rule, self.family, self.world = s, rule, family, world
-        self.stochastic = rule.stochastic or family == "ddpm"
+        self.stochastic = family == "ddpm" or (family == "ddim" and rule.stochastic)
         self.keys = []
         self._key_set = {}
         self.steps = []
@@ -159,7 +159,10 @@ class _Builder:
         return ("noise", key)
 
     def op(self, t, k, *, src, x, eps, z, out, out2=None, save_anchor=False):
-        if self.family == "ddim":
+        if self.family == "euler":     # t = remaining grid intervals: i = N - t
+            c, noisy = euler_op_coeffs(self.s, self.s.N - t, k)
+            fam = _lib.FAMILY_EULER
+        elif self.family == "ddim":
             c, noisy = ddim_op_coeffs(self.s, t, k, self.rule)
             fam = _lib.FAMILY_DDIM
         else:
@@ -174,7 +177,7 @@ class _Builder:
         self.rounds.append(RoundInfo(anchor_t, len(tasks)))
         owner = [None] * len(tasks) if redundant else [i % self.world for i in range(len(tasks))]
         self.steps.append(Eval(r, tasks, dst, owner))
-        if not redundant and self.world > 1:
+        if not redundant and self.world > 1 and tasks:
             self.steps.append(Gather(r, len(tasks)))
         self.eval_count += len(tasks)
         self.max_tasks = max(self.max_tasks, len(tasks))
@@ -198,10 +201,15 @@ def build_parallel(s, plan: BlockPlan, rule: VarianceRule, family: str = "ddim",
     refined state is ever broadcast; each rank only evaluates its own tasks
     (owner = task % world) and the eps rows are all-gathered.  Stand-alone
     anchor evaluations (aggressive initial, conservative per-block,
-    recompute ablation) are single-task rounds computed redundantly."""
-    if family not in ("ddim", "ddpm"):
+    recompute ablation) are single-task rounds computed redundantly.
+
+    family "euler" (parallel.py:324-381): `s` is a SigmaGrid, t counts the
+    remaining grid intervals (N at the start), updates are euler_skip and the
+    velocity tasks at sigma = 0 (t = 0, the aggressive mode's last draft) are
+    dropped, since nothing consumes them (parallel.py:346-349)."""
+    if family not in ("ddim", "ddpm", "euler"):
         raise ValueError(f"unknown update family: {family!r}")
-    T = s.T
+    T = s.N if family == "euler" else s.T
     b = _Builder(s, rule, family, world)
     slot = lambda t: ("traj", T - t)                  # noqa: E731
     mine = lambda i: world == 1 or (i - 1) % world == rank   # noqa: E731  draft i owned?
@@ -235,8 +243,9 @@ def build_parallel(s, plan: BlockPlan, rule: VarianceRule, family: str = "ddim",
             pending_drafts = None
         if pending_drafts is None:
             b.chain(draft_ops(t, k, _lib.SRC_X, slot(t), anchor_eps))
-        tasks = [(i - 1, ("draft", i - 1), t - i) for i in range(1, k + 1)]
-        b.round_(t, tasks, [("eps", i - 1) for i in range(1, k + 1)], redundant=False)
+        live = [i for i in range(1, k + 1) if family != "euler" or t - i > 0]
+        tasks = [(i - 1, ("draft", i - 1), t - i) for i in live]
+        b.round_(t, tasks, [("eps", i - 1) for i in live], redundant=False)
         last = k if plan.mode is Mode.AGGRESSIVE else k + 1
         ops = []
         for i in range(2, last + 1):
@@ -258,6 +267,8 @@ def build_parallel(s, plan: BlockPlan, rule: VarianceRule, family: str = "ddim",
         b.chain(ops)
 
     expected = plan.total_evals
+    if family == "euler" and plan.mode is Mode.AGGRESSIVE:
+        expected -= 1                                 # the sigma = 0 draft of the last block
     if recompute_anchor_eps and plan.mode is Mode.AGGRESSIVE:
         expected += sum(1 for t, _ in plan.blocks if t != T)
     if b.eval_count != expected:
@@ -295,3 +306,16 @@ def build_sequential(s, rule: VarianceRule, family: str = "ddim", subsequence=No
                       z=b.noise(u, Role.TRANSITION), out=("traj", j + 1))])
     return Program("sequential", s.T, len(ts), ts, b.steps, b.rounds, b.keys, 1, 1,
                    b.eval_count, b.stochastic, None, meta={"family": family})
+
+
+def build_sequential_euler(g) -> Program:
+    """IR of sample_euler (sequential.py:116-130): velocity at sigma_i, then
+    x + (sigma_{i+1} - sigma_i) v, for i = 0..N-1; t counts remaining intervals."""
+    N = g.N
+    b = _Builder(g, None, "euler", 1)
+    for j in range(N):
+        t = N - j
+        b.round_(t, [(0, ("traj", j), t)], [("anchor",)], redundant=True)
+        b.chain([b.op(t, 1, src=_lib.SRC_X, x=("traj", j), eps=("anchor",), z=None, out=("traj", j + 1))])
+    return Program("sequential", N, N + 1, list(range(N, -1, -1)), b.steps, b.rounds, b.keys, 1, 1,
+                   b.eval_count, False, None, meta={"family": "euler"})

@@ -138,6 +138,9 @@ def _check_err(err):
     v = int(err.item())
     if v & _lib.ERR_NOISE_WINDOW_BIT:
         raise RuntimeError("ziggurat tail exceeded the noise kernel's lookahead window")
+    if v & _lib.ERR_GM_SIGMA_BIT:
+        from .errors import NonPositiveSigma
+        raise NonPositiveSigma("device velocity evaluated at sigma <= 0")
     if v & _lib.ERR_GM_TIMESTEP_BIT:
         from .errors import TimestepOutOfRange
         raise TimestepOutOfRange("device eps evaluated outside 0..T")

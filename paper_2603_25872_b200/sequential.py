@@ -41,9 +41,19 @@ def sample_ddim(s, d, x_T, rule: VarianceRule, noise: RngStream, subsequence=Non
     return traj
 
 
-def sample_euler(g, gm, x_init):
-    """Euler ODE sampler (sequential.py:116-130): Euler family, next-row scope."""
-    raise NotImplementedError("Euler family (sample_euler) is the next scope row; not built yet")
+def sample_euler(g, gm, x_init) -> Trajectory:
+    """Plain Euler integration of dx/dsigma = (x - x0_hat)/sigma down the grid
+    (sequential.py:116-130): N velocity evaluations (K9, VE mode) and N unit
+    Euler steps (K3), one device program.  Trajectory timesteps count the
+    remaining grid intervals (N at the start, 0 at the end)."""
+    from .denoiser import euler_velocity_core
+    from .program import build_sequential_euler
+    dev = resolve_device(x_init)
+    core = euler_velocity_core(gm, g)
+    run = get_run(("seq", "euler", g.N), lambda: build_sequential_euler(g), g, core, _numel(x_init), dev,
+                  "pcg64", None)
+    traj, _ = execute(run, x_init, 0, None)
+    return traj
 
 
 __all__ = ["Trajectory", "predicted_x0", "sample_ddpm", "sample_ddim", "sample_euler"]

@@ -232,11 +232,18 @@ def predicted_x0_device(s: NoiseSchedule, x_t, eps, t: int):
     return _run_single(c, _lib.FAMILY_PRED_X0, False, x_t, eps, None)
 
 
-def euler_skip(g: SigmaGrid, i: int, k: int, x, v):
-    """x + (sigma_{i+k} - sigma_i) v (transitions.py:182-188)."""
+def euler_op_coeffs(g: SigmaGrid, i: int, k: int):
+    """(c[6], noisy) of the fused Euler step across grid intervals i..i+k:
+    out = x + (sigma_{i+k} - sigma_i) v, the difference formed on the host in
+    fp64 exactly as transitions.py:188; host validation as euler_skip."""
     if k < 1:
         raise InvalidSkip(f"k={k} must be >= 1")
     if i < 0 or i + k > g.N:
         raise IndexOutOfRange(f"(i={i}, k={k}) outside 0 <= i, i+k <= {g.N}")
-    c = [float(g.sigmas[i + k] - g.sigmas[i]), 1.0, 0.0, 0.0, 1.0, 0.0]
+    return [float(g.sigmas[i + k] - g.sigmas[i]), 1.0, 0.0, 0.0, 1.0, 0.0], False
+
+
+def euler_skip(g: SigmaGrid, i: int, k: int, x, v):
+    """x + (sigma_{i+k} - sigma_i) v (transitions.py:182-188)."""
+    c, _ = euler_op_coeffs(g, i, k)
     return _run_single(c, _lib.FAMILY_EULER, False, x, v, None)

@@ -11,7 +11,10 @@ the reference does not travel to the GPU box) and writes:
   traj.npz   sha256 of every trajectory state (bit-exact pin) + selected
              final states for the BASELINE configs' sampler shapes with the
              state-independent and Gaussian-mixture toy denoisers;
-  plans.json plan_blocks for every config.
+  plans.json plan_blocks for every config;
+  euler.npz  Euler family (next-row scope): sigma grids, velocity_oracle
+             values, and sequential / parallel Euler trajectories (sha256 of
+             every state, finals, eval counts, rounds) of the reference.
 Run on numpy 2.3.5 / scipy 1.18.1 / glibc 2.39 (FMA libm variant).
 """
 
@@ -140,8 +143,59 @@ def plans_fixture():
         json.dump(plans, f, indent=0, sort_keys=True)
 
 
+EULER_CASES = [
+    # name, N, sigma_min, sigma_max, rho, dim, sampler, devices
+    ("e16_1d_seq", 16, 0.02, 20.0, 7.0, 1, "seq", 1),
+    ("e16_1d_agg3", 16, 0.02, 20.0, 7.0, 1, "aggressive", 3),
+    ("e16_1d_con3", 16, 0.02, 20.0, 7.0, 1, "conservative", 3),
+    ("e40_4096_seq", 40, 0.002, 80.0, 7.0, 4096, "seq", 1),
+    ("e40_4096_agg4", 40, 0.002, 80.0, 7.0, 4096, "aggressive", 4),
+    ("e40_4096_con4", 40, 0.002, 80.0, 7.0, 4096, "conservative", 4),
+    ("e41_4096_agg8", 41, 0.002, 80.0, 7.0, 4096, "aggressive", 8),
+    ("e9_4096_con8", 9, 0.01, 10.0, 3.0, 4096, "conservative", 8),
+]
+
+
+def euler_fixture():
+    """x_init = sigma_max * derive_noise(INIT) as cli.py:46-47; mixture: the
+    reference's bimodal_1d fixture (tests/conftest.py:17-19) generalised to dim
+    as the configs' toy GM."""
+    out, manifest = {}, []
+    for name, N, smin, smax, rho, dim, sampler, n in EULER_CASES:
+        g = sd.build_sigma_grid(N, smin, smax, rho)
+        gm = gm_toy(dim)
+        stream = sd.RngStream(seed=0)
+        x0 = g.sigmas[0] * sd.derive_noise(stream, N, sd.Role.INIT, dim)
+        if sampler == "seq":
+            traj, rep = sd.sample_euler(g, gm, x0), []
+        else:
+            traj, rep = sd.run_parallel_euler(g, gm, x0, n, sd.Mode(sampler))
+        out[f"{name}_sigmas"] = g.sigmas
+        out[f"{name}_x0"] = x0
+        out[f"{name}_sha"] = np.array([_sha(x) for _, x in traj.states])
+        out[f"{name}_t"] = np.array(traj.timesteps())
+        out[f"{name}_final"] = traj.final
+        out[f"{name}_mid"] = traj.states[len(traj.states) // 2][1]
+        manifest.append({"name": name, "N": N, "sigma_min": smin, "sigma_max": smax, "rho": rho, "dim": dim,
+                         "sampler": sampler, "devices": n, "eval_count": traj.eval_count, "rounds": len(rep)})
+    # velocity values: a state per sigma of the 4096-D grid
+    g = sd.build_sigma_grid(40, 0.002, 80.0, 7.0)
+    gm = gm_toy(4096)
+    xs, vs = [], []
+    for i in (0, 7, 20, 33, 39):
+        x = g.sigmas[i] * sd.derive_noise(sd.RngStream(seed=5), i + 1, sd.Role.DRAFT, 4096)
+        xs.append(x)
+        vs.append(sd.velocity_oracle(gm, x, float(g.sigmas[i])))
+    out["vel_sigmas"] = np.array([g.sigmas[i] for i in (0, 7, 20, 33, 39)])
+    out["vel_x"] = np.array(xs)
+    out["vel_v"] = np.array(vs)
+    out["manifest"] = np.array(json.dumps(manifest))
+    np.savez_compressed(os.path.join(HERE, "euler.npz"), **out)
+
+
 if __name__ == "__main__":
     noise_fixture()
     traj_fixture()
     plans_fixture()
+    euler_fixture()
     print("golden fixtures written to", HERE)

@@ -122,6 +122,17 @@ int drs_gm_velocity(const double* const* xs, const int32_t* idx, int n_rows, int
                     const double* sigmas, int N, const double* means, const double* log_w,
                     const double* var, int n_comp, double* const* out, int* err, void* stream);
 
+/* ---- quality metrics (K10, next-row scope: metrics.py:42-89) ---------------- */
+/* out[i] = |X[i,:]|^2 for a row-major (n, dim) fp64 matrix (squared row norms). */
+int drs_row_sqnorm(const double* X, int n, int dim, double* out, void* stream);
+/* Gaussian-kernel MMD partial sums (mmd_gaussian, metrics.py:72-89) without the
+ * n x m kernel matrix: partial[by * gx + bx] = sum over the 64 x 64 pair tile
+ * (bx, by) of exp(-gamma * max(na[i] + nb[j] - 2 A_i . B_j, 0)), pairs i == j
+ * skipped when same != 0 (A == B).  gx = ceil(m/64), gy = ceil(n/64) <= 65535;
+ * the caller sums the gx*gy partials in index order (bit-reproducible). */
+int drs_mmd_partials(const double* A, const double* na, int n, const double* B, const double* nb, int m,
+                     int dim, double gamma, int same, double* partial, void* stream);
+
 /* Copy rows: out[r][0..D) = src[r][0..D) (DEVICE pointer arrays). */
 int drs_copy_rows(const double* const* src, double* const* out, int n_rows, int64_t D,
                   void* stream);

@@ -27,6 +27,7 @@ SOURCES = {                      # source -> extra flags
     "chain.cu": EXACT,
     "gm_eps.cu": EXACT,
     "misc.cu": EXACT,
+    "metrics.cu": EXACT,
     "gemm_tc.cu": [],
     "net_ops.cu": [],
     "attn_tc.cu": [],

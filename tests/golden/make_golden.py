@@ -14,7 +14,10 @@ the reference does not travel to the GPU box) and writes:
   plans.json plan_blocks for every config;
   euler.npz  Euler family (next-row scope): sigma grids, velocity_oracle
              values, and sequential / parallel Euler trajectories (sha256 of
-             every state, finals, eval counts, rounds) of the reference.
+             every state, finals, eval counts, rounds) of the reference;
+  metrics.json sliced_w2 / mmd_gaussian / mmd_permutation_threshold of the
+             reference on seeded sample sets (inputs regenerated from the
+             seeds by metric_inputs()).
 Run on numpy 2.3.5 / scipy 1.18.1 / glibc 2.39 (FMA libm variant).
 """
 
@@ -193,9 +196,27 @@ def euler_fixture():
     np.savez_compressed(os.path.join(HERE, "euler.npz"), **out)
 
 
+from metric_cases import METRIC_CASES, metric_inputs  # noqa: E402
+
+
+def metrics_fixture():
+    vals = []
+    for name, seed, (na, nb, dim), shift, P, wseed, bw in METRIC_CASES:
+        a, b = metric_inputs(seed, na, nb, dim, shift)
+        A, B = sd.SampleSet(a), sd.SampleSet(b)
+        vals.append({"name": name, "seed": seed, "n_a": na, "n_b": nb, "dim": dim, "shift": shift,
+                     "projections": P, "w2_seed": wseed, "bandwidth": bw,
+                     "sliced_w2": sd.sliced_w2(A, B, projections=P, seed=wseed),
+                     "mmd": sd.mmd_gaussian(A, B, bw),
+                     "threshold": sd.mmd_permutation_threshold(A, B, bw, permutations=20, seed=wseed)})
+    with open(os.path.join(HERE, "metrics.json"), "w") as f:
+        json.dump(vals, f, indent=1)
+
+
 if __name__ == "__main__":
     noise_fixture()
     traj_fixture()
     plans_fixture()
     euler_fixture()
+    metrics_fixture()
     print("golden fixtures written to", HERE)

@@ -15,6 +15,9 @@ the reference does not travel to the GPU box) and writes:
   euler.npz  Euler family (next-row scope): sigma grids, velocity_oracle
              values, and sequential / parallel Euler trajectories (sha256 of
              every state, finals, eval counts, rounds) of the reference;
+  cli/       the reference CLI's own output files (samples CSV, rounds CSV,
+             JSON report) for the configs cli/*.cfg, written by its
+             `sample` command in a scratch directory;
   metrics.json sliced_w2 / mmd_gaussian / mmd_permutation_threshold of the
              reference on seeded sample sets (inputs regenerated from the
              seeds by metric_inputs()).
@@ -213,7 +216,27 @@ def metrics_fixture():
         json.dump(vals, f, indent=1)
 
 
+def cli_fixture():
+    import shutil
+    import tempfile
+    from skipdiff.cli import main as cli_main
+    src = os.path.join(HERE, "cli")
+    with tempfile.TemporaryDirectory() as tmp:
+        for cfg in sorted(f for f in os.listdir(src) if f.endswith(".cfg")):
+            shutil.copy(os.path.join(src, cfg), tmp)
+            cwd = os.getcwd()
+            os.chdir(tmp)
+            try:
+                assert cli_main(["sample", "--config", cfg]) == 0
+            finally:
+                os.chdir(cwd)
+        for f in os.listdir(tmp):
+            if not f.endswith(".cfg"):
+                shutil.copy(os.path.join(tmp, f), src)
+
+
 if __name__ == "__main__":
+    cli_fixture()
     noise_fixture()
     traj_fixture()
     plans_fixture()

@@ -122,6 +122,15 @@ int drs_gm_velocity(const double* const* xs, const int32_t* idx, int n_rows, int
                     const double* sigmas, int N, const double* means, const double* log_w,
                     const double* var, int n_comp, double* const* out, int* err, void* stream);
 
+/* ---- Perturbed-denoiser ablation (next-row scope) ----------------------------- */
+/* keys[r] = the noise key of denoiser.py:224-231's perturbation of state xs[r]
+ * (fp64, D) at timestep ts[r] (DEVICE int32): BLAKE2b-64(b"perturb" || t ||
+ * round(x / quantum) as int64) as a one-value drs_key, consumed by
+ * drs_noise_fill to draw the perturbation (default_rng(digest).standard_normal).
+ * quantum = 1e-8 in the reference.  xs: DEVICE array of n_rows pointers. */
+int drs_perturb_keys(const double* const* xs, const int32_t* ts, int n_rows, int64_t D, double quantum,
+                     drs_key* keys, void* stream);
+
 /* ---- quality metrics (K10, next-row scope: metrics.py:42-89) ---------------- */
 /* out[i] = |X[i,:]|^2 for a row-major (n, dim) fp64 matrix (squared row norms). */
 int drs_row_sqnorm(const double* X, int n, int dim, double* out, void* stream);

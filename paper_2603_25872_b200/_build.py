@@ -28,6 +28,7 @@ SOURCES = {                      # source -> extra flags
     "gm_eps.cu": EXACT,
     "misc.cu": EXACT,
     "metrics.cu": EXACT,
+    "perturb.cu": EXACT,
     "gemm_tc.cu": [],
     "net_ops.cu": [],
     "attn_tc.cu": [],

@@ -10,9 +10,10 @@ The same kinds exist here, evaluated by libdrs kernels:
   Counting(inner)        -> host-side counter
   NetworkEps(net)        -> a random-init denoiser network (new; no reference)
 
-`Perturbed` (blake2b hash of the quantised state, denoiser.py:224-231) needs
-the state bytes on the host every call; it is a robustness probe outside the
-hot path and raises NotImplementedError here.
+`Perturbed` (denoiser.py:191-201,224-231) runs on device too: a BLAKE2b
+kernel hashes the quantised state into a noise key in HBM, K1 draws the
+pseudo-noise from it and a K3 chain adds scale * noise to the eps rows, so a
+perturbed run stays one captured program (PerturbPlan below).
 """
 
 import time
@@ -149,6 +150,80 @@ class NetworkEps:
 
 
 Denoiser = AnalyticEps | StateIndependent | Perturbed | Latency | Counting | NetworkEps
+
+
+# ------------------------------------------------------------ Perturbed ---
+PERTURB_QUANTUM = 1e-8        # denoiser.py:24
+
+
+def perturb_scales(d) -> list:
+    """Scales of the Perturbed layers of a wrapper stack, innermost first;
+    zero scales are identity (denoiser.py:253-256) and dropped."""
+    out = []
+    while True:
+        if isinstance(d, Perturbed):
+            if d.scale != 0.0:
+                out.append(float(d.scale))
+            d = d.inner
+        elif isinstance(d, (Latency, Counting)):
+            d = d.inner
+        else:
+            return out[::-1]
+
+
+class _DevKeys:
+    """drs_key rows already in HBM (written by drs_perturb_keys)."""
+
+    def __init__(self, dev, n):
+        self.dev, self.n = dev, n
+
+
+class PerturbPlan:
+    """Device resources adding every Perturbed layer's pseudo-noise to eps rows:
+    outs[i] += scale * default_rng(blake2b(state_i, t_i)).standard_normal(D)
+    for each scale, innermost first (denoiser.py:224-231,253-256)."""
+
+    def __init__(self, scales, xs, ts, outs, device):
+        import torch
+        from .transitions import make_op, ops_to_device
+        self.n, self.D = len(xs), int(xs[0].numel())
+        self.xs = _ptr_array(xs, device)
+        self.ts = torch.tensor([int(t) for t in ts], dtype=torch.int32, device=device)
+        self.keys = torch.zeros(self.n * _lib.ctypes.sizeof(_lib.DrsKey), dtype=torch.uint8, device=device)
+        self.noise = torch.empty(self.n, self.D, dtype=torch.float64, device=device)
+        ops = []
+        for i in range(self.n):
+            for j, sc in enumerate(scales):       # out = eps + scale * noise (K3 euler form), chained
+                ops.append(make_op([sc, 1.0, 0.0, 0.0, 1.0, 0.0], _lib.FAMILY_EULER, False,
+                                   src=_lib.SRC_X if j == 0 else _lib.SRC_CUR, x=outs[i] if j == 0 else None,
+                                   eps=self.noise[i], out=outs[i]))
+        self.n_ops = len(ops)
+        self.ops = ops_to_device(ops, device)
+
+    def launch(self, err, stream=None):
+        from .rng import fill_streams
+        L = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        _lib.check(L.drs_perturb_keys(self.xs.data_ptr(), self.ts.data_ptr(), self.n, self.D, PERTURB_QUANTUM,
+                                      self.keys.data_ptr(), sp), "drs_perturb_keys")
+        fill_streams(_DevKeys(self.keys, self.n), self.D, self.noise, "pcg64", err=err, stream=stream)
+        size = _lib.ctypes.sizeof(_lib.DrsOp)
+        for off in range(0, self.n_ops, 64):
+            _lib.check(L.drs_skip_chain(self.ops.data_ptr() + off * size, min(64, self.n_ops - off), self.D, sp),
+                       "drs_skip_chain")
+
+
+def apply_perturbations(scales, x, t: int, value):
+    """value (eps of state x at t, CUDA fp64) + the Perturbed layers' noise, in place."""
+    import torch
+    from .rng import _check_err
+    if not scales:
+        return value
+    err = torch.zeros(1, dtype=torch.int32, device=value.device)
+    plan = PerturbPlan(scales, [x.reshape(-1)], [t], [value.reshape(-1)], value.device)
+    plan.launch(err)
+    _check_err(err)
+    return value
 
 
 # ------------------------------------------------------------ oracles -----
@@ -302,9 +377,15 @@ def evaluate(d, s: NoiseSchedule, x, t: int, clock: VirtualClock | None = None):
         return state_independent_eps(d.seed, t, d.dim,
                                      device=dev if dev is not None and dev.type == "cuda" else None)
     if isinstance(d, Perturbed):
+        value = evaluate(d.inner, s, x, t, clock)
         if d.scale == 0.0:
-            return evaluate(d.inner, s, x, t, clock)
-        raise NotImplementedError("Perturbed with scale > 0 hashes host state bytes; not on the B200 path")
+            return value
+        import torch
+        from .transitions import _device_of, as_device
+        dev = _device_of(x, value)
+        xd = as_device(x, dev, torch.float64)
+        out = as_device(value, dev, torch.float64).clone().reshape(xd.shape)
+        return apply_perturbations([d.scale], xd, t, out)
     if isinstance(d, Latency):
         if clock is not None:
             clock.charge(d.model.eval_time_ms)

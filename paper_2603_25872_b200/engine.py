@@ -18,8 +18,8 @@ import math
 import torch
 
 from . import _lib
-from .denoiser import (AnalyticEps, Counting, EulerVelocity, Latency, NetworkEps, Perturbed, StateIndependent,
-                       latency_of, state_independent_key)
+from .denoiser import (AnalyticEps, Counting, EulerVelocity, Latency, NetworkEps, Perturbed, PerturbPlan,
+                       StateIndependent, latency_of, perturb_scales, state_independent_key)
 from .program import Chain, Eval, Gather, Noise, Program
 from .rng import _STREAM_SALT, _SEED_MASK48, GENERATORS, _KeyBuffer, entropy_key
 from .transitions import ops_to_device
@@ -37,9 +37,7 @@ def unwrap(d):
         elif isinstance(d, Counting):
             counters.append(d)
             d = d.inner
-        elif isinstance(d, Perturbed):
-            if d.scale != 0.0:
-                raise NotImplementedError("Perturbed(scale > 0) is not on the B200 path")
+        elif isinstance(d, Perturbed):      # applied after the core eval (PerturbPlan)
             d = d.inner
         else:
             return d, lat, counters
@@ -80,6 +78,7 @@ class DeviceRun:
             raise ValueError(f"program built for world {prog.world}, comm has {self.comm.size}")
         self.generator = generator
         self.core, self.eval_ms, self.counters = unwrap(d)
+        self.perturb = perturb_scales(d)
         self.overhead_ms = (latency_of(d).dispatch_overhead_ms if latency_of(d) else 0.0)
         core = self.core
         if isinstance(core, (AnalyticEps, StateIndependent, EulerVelocity)):
@@ -100,6 +99,8 @@ class DeviceRun:
             self.eps_dtype = torch.float32
         else:
             raise TypeError(f"unknown denoiser kind: {type(core).__name__}")
+        if self.perturb and self.eps_dtype != torch.float64:
+            raise NotImplementedError("Perturbed wraps the fp64 toy denoisers (denoiser.py:191-201)")
         self._alloc()
         self._lower()
         self.graph = None
@@ -178,7 +179,12 @@ class DeviceRun:
             elif isinstance(st, Eval):
                 local = [(tk, dst) for tk, dst, own in zip(st.tasks, st.dst, st.owner)
                          if own is None or own == rank]
-                self.launches.append(("eval", (st.round, self._lower_eval(local))))
+                low = self._lower_eval(local)
+                if low is not None and self.perturb:
+                    low = ("pert", low, PerturbPlan(self.perturb, [self.buf(src) for (_, src, _), _ in local],
+                                                    [t for (_, _, t), _ in local],
+                                                    [self.buf(dst) for _, dst in local], self.device))
+                self.launches.append(("eval", (st.round, low)))
             elif isinstance(st, Gather):
                 self.launches.append(("gather", st.round))
             elif isinstance(st, Noise):
@@ -203,6 +209,8 @@ class DeviceRun:
             low = payload[1]
             if low is None:
                 return 0
+            if low[0] == "pert":
+                low = low[1]
             if low[0] in ("gm", "gmv"):
                 return low[1]["n"] * self.dim * 8 * (2 + low[1]["n_comp"])
             if low[0] == "copy":
@@ -264,6 +272,10 @@ class DeviceRun:
         self.seeds.copy_(self._seed_host, non_blocking=True)
 
     def _launch_eval(self, payload, stream):
+        if payload[0] == "pert":
+            self._launch_eval(payload[1], stream)
+            payload[2].launch(self.err)
+            return
         kind, a = payload
         L = _lib.lib()
         if kind == "gm":

@@ -19,7 +19,7 @@ import os
 import torch
 
 from . import _lib
-from .denoiser import AnalyticEps, StateIndependent, evaluate, latency_of
+from .denoiser import AnalyticEps, StateIndependent, apply_perturbations, evaluate, latency_of, perturb_scales
 from .engine import Comm, unwrap
 from .errors import InvalidPlanParams, WorkerFailure
 from .program import BlockPlan, Mode, build_parallel, plan_blocks
@@ -73,9 +73,14 @@ def execute_round(d, s, tasks: list, devices: int, *, anchor_t: int, pool=None, 
     if eval_ms > 0 and tasks:          # all tasks' latency occupies the GPU concurrently
         _lib.check(_lib.lib().drs_spin(eval_ms * 1000.0, len(tasks), _lib.stream_ptr()), "drs_spin")
     results, error = [None] * len(tasks), None
+    scales = perturb_scales(d)
     for i, (x, t) in enumerate(tasks):
         try:
             results[i] = evaluate(core, s, x, t)
+            if scales:
+                results[i] = apply_perturbations(scales, torch.as_tensor(x, dtype=torch.float64,
+                                                                         device=results[i].device),
+                                                 t, results[i].clone())
         except Exception as exc:      # drain the round before raising (parallel.py:168-179)
             if error is None:
                 error = exc

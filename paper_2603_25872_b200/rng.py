@@ -107,7 +107,7 @@ def fill_streams(keys, n: int, out, generator: str = "pcg64", seeds=None, err=No
     tensor of shape (len(keys), >= n), row-contiguous."""
     import torch
     device = out.device
-    kb = keys if isinstance(keys, _KeyBuffer) else _KeyBuffer(keys, device)
+    kb = keys if hasattr(keys, "dev") else _KeyBuffer(keys, device)     # keys already in HBM, or a host list
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=device)
     ld = out.stride(0) if out.dim() == 2 else n

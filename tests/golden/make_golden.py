@@ -18,6 +18,9 @@ the reference does not travel to the GPU box) and writes:
   cli/       the reference CLI's own output files (samples CSV, rounds CSV,
              JSON report) for the configs cli/*.cfg, written by its
              `sample` command in a scratch directory;
+  perturb.npz Perturbed-denoiser ablation: BLAKE2b digests and
+             _perturbation draws of seeded states, and Perturbed(SI)
+             trajectories (sha256 per state) of the parallel schedulers;
   metrics.json sliced_w2 / mmd_gaussian / mmd_permutation_threshold of the
              reference on seeded sample sets (inputs regenerated from the
              seeds by metric_inputs()).
@@ -216,6 +219,53 @@ def metrics_fixture():
         json.dump(vals, f, indent=1)
 
 
+PERTURB_TRAJ = [
+    # name, T, D, sampler, devices, family, rule, scale, seed
+    ("p_agg3", 20, 64, "aggressive", 3, "ddim", "ddpm", 0.05, 2),
+    ("p_con4", 17, 256, "conservative", 4, "ddpm", "det", 0.2, 3),
+    ("p_seq", 12, 64, "seq_ddim", 1, "ddim", "det", 0.1, 1),
+]
+
+
+def perturb_fixture():
+    import hashlib as hl
+    from skipdiff import denoiser as sdd
+    out = {}
+    rng = np.random.default_rng(99)
+    xs, ts, digs, pert = [], [], [], []
+    for i, (D, t) in enumerate([(1, 0), (5, 7), (64, 50), (1000, 3), (4096, 250)]):
+        x = rng.normal(size=D) * (10.0 ** (i - 2))
+        q = np.round(np.asarray(x, dtype=float) / sdd._PERTURB_QUANTUM).astype(np.int64)
+        dig = hl.blake2b(sdd._PERTURB_SALT + int(t).to_bytes(8, "little", signed=True) + q.tobytes(),
+                         digest_size=8).digest()
+        out[f"x{i}"] = x
+        out[f"pert{i}"] = sdd._perturbation(x, t, 0.3)
+        ts.append(t)
+        digs.append(int.from_bytes(dig, "little"))
+    out["ts"] = np.array(ts)
+    out["digests"] = np.array(digs, dtype=np.uint64)
+    manifest = []
+    for name, T, D, sampler, n, fam, rule_s, scale, seed in PERTURB_TRAJ:
+        s_ = sd.default_schedule(T)
+        rule = sd.VarianceRule.deterministic() if rule_s == "det" else sd.VarianceRule.ddpm_induced()
+        den = sd.Perturbed(sd.StateIndependent(seed=11, dim=D), scale)
+        stream = sd.RngStream(seed=seed)
+        x_T = sd.derive_noise(stream, T, sd.Role.INIT, D)
+        if sampler == "aggressive":
+            traj, rep = sd.run_aggressive(s_, den, x_T, n, rule, stream, update_family=fam)
+        elif sampler == "conservative":
+            traj, rep = sd.run_conservative(s_, den, x_T, n, rule, stream, update_family=fam)
+        else:
+            traj, rep = sd.sample_ddim(s_, den, x_T, rule, stream), []
+        out[f"{name}_sha"] = np.array([_sha(x) for _, x in traj.states])
+        out[f"{name}_final"] = traj.final
+        manifest.append({"name": name, "T": T, "D": D, "sampler": sampler, "devices": n, "family": fam,
+                         "rule": rule_s, "scale": scale, "seed": seed, "si_seed": 11,
+                         "eval_count": traj.eval_count, "rounds": len(rep)})
+    out["manifest"] = np.array(json.dumps(manifest))
+    np.savez_compressed(os.path.join(HERE, "perturb.npz"), **out)
+
+
 def cli_fixture():
     import shutil
     import tempfile
@@ -242,4 +292,5 @@ if __name__ == "__main__":
     plans_fixture()
     euler_fixture()
     metrics_fixture()
+    perturb_fixture()
     print("golden fixtures written to", HERE)

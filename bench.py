@@ -56,6 +56,28 @@ def _args():
     return ap.parse_args()
 
 
+def _gemm_replay_ms(rec, dev, warm=3, reps=5):
+    """ms per replay of a CUDA graph holding every recorded drs_gemm launch."""
+    import torch
+    from paper_2603_25872_b200 import _lib
+    st = torch.cuda.Stream(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st):
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(g, stream=st):
+            for _, args in rec:
+                _lib.check(_lib.lib().drs_gemm(_lib.ctypes.byref(args), st.cuda_stream), "drs_gemm")
+        for _ in range(warm):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / reps
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -324,6 +346,7 @@ def main():
     peaks = _peaks()
     timers = []
     netops.TIMERS = [] if net_cfg else None
+    netops.GEMM_RECORD = [] if net_cfg else None
     sampler.stage(2000)
     torch.cuda.synchronize(dev)
     sampler.run.enqueue(timers=timers)
@@ -337,14 +360,22 @@ def main():
     if net_cfg:
         gt = netops.TIMERS
         netops.TIMERS = None
-        g_ms = sum(e0.elapsed_time(e1) for _, e0, e1, _ in gt)
-        g_flops = sum(f for f, _, _, _ in gt)
+        rec = netops.GEMM_RECORD
+        netops.GEMM_RECORD = None
+        g_ms_events = sum(e0.elapsed_time(e1) for _, e0, e1, _ in gt)
+        g_flops = sum(f for f, _ in rec)
+        # the image's GEMM launches (same arguments and buffers) replayed back to
+        # back from one CUDA graph: device time of the tensor-core kernels alone
+        g_ms = _gemm_replay_ms(rec, dev)
         achieved = g_flops / (g_ms * 1e-3) / 1e12
         peak = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
         ev_ms = classes.get("eval_net", {"ms": 0.0})["ms"]
         roofline = {"bound": "tensor", "kernel": "gemm_bf16_tc_kernel (tcgen05.mma, TMA, TMEM)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": None, "gemm_ms_per_image": g_ms, "gemm_tflop_per_image": g_flops / 1e12,
+                    "gemm_ms_per_image_eager_events": g_ms_events,
+                    "method": "all GEMM launches of one image (recorded drs_gemm arguments) replayed from one "
+                              "CUDA graph, 3 warm + 5 timed replays, CUDA events on the replay stream",
                     "gemm_launches_per_image": len(gt), "gemm_share_of_eval_time": g_ms / ev_ms if ev_ms else None,
                     "network_tflop_per_eval": (net.flops or 0) / 1e12 if cfg["net"] != "dit" else
                     net.cfg.flops_per_image() / 1e12,

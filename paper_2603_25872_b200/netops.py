@@ -67,6 +67,8 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     g.bn, g.split = bn, split
     if conv is not None:
         g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
+    if GEMM_RECORD is not None:
+        GEMM_RECORD.append((2.0 * M * N * K, _lib.DrsGemmArgs.from_buffer_copy(g)))
     if TIMERS is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -83,6 +85,8 @@ BN_CHOICES = (64, 128, 160, 192, 256)
 _TABLE_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gemm_table.json")
 _TABLE = None
 SHAPES = None      # when a list: linear() appends (M, N, K, act, res_f32, has_res, out_f32, conv) (tuning)
+GEMM_RECORD = None  # when a list: linear() appends (flops, drs_gemm_args copy) -- bench.py replays them
+                    # back to back in one CUDA graph to time the tensor-core kernels alone
 
 
 def _table():

@@ -10,6 +10,7 @@
 #ifndef DRS_NET_H_
 #define DRS_NET_H_
 #include <stdint.h>
+#include <stddef.h>
 #include "drs.h"
 
 #ifdef __cplusplus

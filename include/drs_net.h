@@ -56,6 +56,11 @@ typedef struct drs_gemm_args {
    * input [conv_N, conv_H, conv_W, conv_C] (M = N*H*W, K = 9*C, weights
    * (Cout, ky, kx, C)); C % 64 == 0, W a power of two <= 128. */
   int conv_N, conv_H, conv_W, conv_C;
+  /* 1: run the tile on a CTA PAIR (tcgen05.mma.cta_group::2, M = 256 per pair,
+   * each CTA loads its 128 A rows and half of the B tile -> (128 + bn/2) x 128 B
+   * of operand ingest per SM per k-block instead of (128 + bn) x 128 B).
+   * Needs M >= 256 and split == 1; otherwise ignored.  0: one CTA per tile. */
+  int cta_pair;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
 

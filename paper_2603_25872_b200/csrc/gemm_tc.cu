@@ -24,6 +24,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string.h>
+#include <stdlib.h>
 #include "drs_net.h"
 #include "pdl.cuh"
 #include "tc_common.cuh"
@@ -515,6 +516,229 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   if (warp == 1) tc::tmem_dealloc<kTmemCols>(tmem_base);
 }
 
+// ---- 2-SM (CTA pair) variant: tcgen05.mma.cta_group::2, M = 256 per pair ----
+// The two CTAs of a cluster share one 256 x BN output tile: CTA r owns rows
+// r*128 .. r*128+127 (its own A tile and TMEM accumulator) and loads HALF of
+// the B tile (BN/2 rows, at the same smem offset in both CTAs); the leader's
+// single thread issues the M=256 MMAs, which read A from each CTA's smem and
+// the two B halves across the pair.  Per-SM operand ingest per k-block drops
+// from (128 + BN) x 128 B to (128 + BN/2) x 128 B -- the bound of the 1-SM
+// kernel on the UNet shapes.  Barriers: every TMA of the pair completes on
+// the LEADER's full barrier; the leader's MMA commits multicast to both CTAs'
+// empty / tfull barriers; both CTAs' epilogue warps arrive on the leader's
+// tempty barrier (remote arrive through DSMEM).
+template <int BN, int kStages>
+struct PairSmem {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;         // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStgOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
+  static constexpr int kBytes = kBarOffset + (2 * kStages + 4) * 8 + 16 + 1024;
+  static_assert(kBytes <= 227 * 1024, "GEMM pair shared memory plan exceeds 227 KB");
+};
+
+__device__ __forceinline__ void tma_load_2d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1) {
+  // completes on the leader's barrier: clear the peer bit of the shared::cluster address
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                                 int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2),
+         "r"(c3) : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {      // both CTAs' barrier
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(tc::smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+__device__ __forceinline__ uint32_t pair_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {   // arrive on rank 0's copy of `bar`
+  uint32_t a = tc::smem_u32(bar), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(r) : "memory");
+}
+__device__ __forceinline__ void pair_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BN, int kStages>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                 const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K, EpiParams ep, ConvGeom cv) {
+  using S = PairSmem<BN, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;       // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;            // [2] (leader's counts both CTAs' epilogues)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)pair_rank();
+  const int pm_tiles = (M + 2 * kBM - 1) / (2 * kBM), n_tiles = (N + BN - 1) / BN;
+  const int num_kb = (K + kBK - 1) / kBK;
+  const int num_tiles = pm_tiles * n_tiles;
+  const int t0 = blockIdx.x / 2, tstep = gridDim.x / 2;
+  constexpr uint32_t kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
+  constexpr uint32_t kIdesc = tc::idesc_bf16_f32(2 * kBM, BN);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmap_a);
+    tc::tma_prefetch(&tmap_b);
+    if (ep.tma_store) tc::tma_prefetch(&tmap_c);
+    for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], 2 * kEpiWarps); }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {                                  // both CTAs, same warp and slot (cta_group::2 allocation)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(tc::smem_u32(tmem_slot)), "n"(kTmemCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  pair_sync();                                      // barriers and TMEM of both CTAs are ready
+  tc::tc_fence_after();
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, half of B) ----------------
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = t0; tile < num_tiles; tile += tstep) {
+        const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
+        const int m0 = (pmt * 2 + rank) * kBM;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          if (cv.on) {
+            const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
+            const int ky = tap / 3, kx = tap - ky * 3;
+            const int hw = cv.H * cv.W;
+            const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+            tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+          } else {
+            tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
+          }
+          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + rank * (BN / 2));
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = t0; tile < num_tiles; tile += tstep, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          tc::mbar_wait(&full_bar[stage], phase);
+          tc::tc_fence_after();
+          if (tc::elect_one()) {
+            const uint8_t* sa = smem + stage * S::kStageBytes;
+            const uint64_t da = tc::smem_desc_sw128(sa);
+            const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb > 0 || k > 0) ? 1u : 0u);
+            mma_commit_pair(&empty_bar[stage]);
+            if (kb == num_kb - 1) mma_commit_pair(&tfull_bar[acc]);
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9 of both CTAs: own 128 rows) ----------------
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const bool geglu = ep.act == DRS_ACT_GEGLU;
+    const int pitch = (geglu ? 16 : 32) * (ep.out_f32 ? 4 : 2);
+    const bool dbl = pitch * 32 <= kStgBytes / 2;
+    uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
+    int buf = 0;
+    int it = 0;
+    for (int tile = t0; tile < num_tiles; tile += tstep, ++it) {
+      const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
+      const int mrow0 = (pmt * 2 + rank) * kBM;
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int row = mrow0 + quad * 32 + lane;
+#pragma unroll 1
+      for (int c = half; c < BN / 32; c += 2) {
+        const int n0 = nt * BN + c * 32;
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
+        tc::tmem_ld_wait();
+        if (n0 >= N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (ep.tma_store) {
+          epi_math32(ep, M, N, row, n0, v);
+          if (lane == 0) {
+            if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          }
+          __syncwarp();
+          uint8_t* sb = stg + buf * (kStgBytes / 2);
+          stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
+          fence_async_smem_g();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_c, sb, geglu ? n0 / 2 : n0, mrow0 + quad * 32);
+            bulk_commit();
+          }
+          if (dbl) buf ^= 1;
+        } else {
+          epilogue32(ep, M, N, row, n0, v);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
+    }
+    if (ep.tma_store && lane == 0) bulk_wait_all();
+  }
+  __syncwarp();
+  tc::tc_fence_before();
+  pair_sync();                                      // all MMAs / epilogues of the pair are done
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "n"(kTmemCols) : "memory");
+  }
+}
+
 // ------------------------------------------------------------ host side ---
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -659,6 +883,50 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+template <int BN, int kStages>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, int M, int N, int K,
+                       const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
+  using S = PairSmem<BN, kStages>;
+  auto kern = gemm_pair_kernel<BN, kStages>;
+  static int cap = 0;
+  if (!cap) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
+      return DRS_ERR_CUDA;
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(128);
+    q.blockDim = dim3(kGemmThreads);
+    q.dynamicSmemBytes = S::kBytes;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = 2;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms() / 2;
+    cudaGetLastError();
+    cap = n;
+  }
+  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (tiles < cap ? tiles : cap));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = S::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, M, N, K, ep, cv);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
 static int max_clusters_bn(int bn, int split) {
   switch (bn) {
     case 64: return max_clusters<64, 8>(split);
@@ -757,7 +1025,9 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
     return DRS_ERR_CUDA;
   }
-  if (!make_tmap(&tb, g->B, N, K, g->ldb, bn)) return DRS_ERR_CUDA;
+  // 2-SM pair mode: M >= 256, no split-K
+  const bool pair = g->cta_pair > 0 && split == 1 && M >= 2 * kBM;
+  if (!make_tmap(&tb, g->B, N, K, g->ldb, pair ? bn / 2 : bn)) return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
@@ -772,6 +1042,13 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
+  if (pair) {
+    if (bn == 64) return launch_pair<64, 8>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 128) return launch_pair<128, 8>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 160) return launch_pair<160, 7>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 192) return launch_pair<192, 6>(ta, tb, tcm, M, N, K, ep, cv, st);
+    return launch_pair<256, 6>(ta, tb, tcm, M, N, K, ep, cv, st);
+  }
   if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, tcm, M, N, K, split, ep, cv, st);
   else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, tcm, M, N, K, split, ep, cv, st);
   else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, tcm, M, N, K, split, ep, cv, st);

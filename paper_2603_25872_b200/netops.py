@@ -25,7 +25,7 @@ def _ptr(t):
 
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
-           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None):
+           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group."""
@@ -63,8 +63,11 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
         SHAPES.append((M, N, K, act, residual is not None and residual.dtype == torch.float32,
                        residual is not None, out.dtype == torch.float32, None if conv is None else tuple(conv)))
     if bn == 0 or split == 0:                    # tuned table, else the library cost model
-        bn, split = pick(M, N, K, bn, split, conv is not None)
+        bn, split, tpair = pick3(M, N, K, bn, split, conv is not None)
+        if pair is None:
+            pair = tpair
     g.bn, g.split = bn, split
+    g.cta_pair = 1 if pair else 0
     if conv is not None:
         g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
     if GEMM_RECORD is not None:
@@ -104,14 +107,24 @@ def table_key(M, N, K, conv=False):
     return f"{M}x{N}x{K}" + (":conv" if conv else "")
 
 
-def pick(M, N, K, bn=0, split=0, conv=False):
-    """(bn, split) for this GEMM: explicit values win; otherwise the measured
-    B200 table (tools/gemm_tune.py -> gemm_table.json) for shapes the networks
-    issue, else the library's cost model (drs_gemm_pick)."""
+def pick3(M, N, K, bn=0, split=0, conv=False):
+    """(bn, split, cta_pair) for this GEMM: explicit bn/split win; otherwise the
+    measured B200 table (tools/gemm_tune.py -> gemm_table.json) for shapes the
+    networks issue, else the library's cost model (drs_gemm_pick, no pair)."""
     if bn == 0 and split == 0:
         hit = _table().get(table_key(M, N, K, conv))
         if hit is not None:
-            return hit
+            return (hit[0], hit[1], bool(hit[2]) if len(hit) > 2 else False)
+    b, sp = pick(M, N, K, bn, split, conv)
+    return b, sp, False
+
+
+def pick(M, N, K, bn=0, split=0, conv=False):
+    """(bn, split) for this GEMM (see pick3)."""
+    if bn == 0 and split == 0:
+        hit = _table().get(table_key(M, N, K, conv))
+        if hit is not None:
+            return tuple(hit[:2])
     b, sp = _lib.ctypes.c_int(bn), _lib.ctypes.c_int(split)
     _lib.check(_lib.lib().drs_gemm_pick(M, N, K, _lib.ctypes.byref(b), _lib.ctypes.byref(sp)), "drs_gemm_pick")
     return b.value, sp.value

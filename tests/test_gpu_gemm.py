@@ -119,3 +119,26 @@ def test_implicit_conv3x3_splitk(cuda, split):
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Co)
     err = (y - ref).abs().max().item()
     assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M,N,K,bn,conv", [(1000, 640, 576, 160, None), (300, 256, 1152, 128, None),
+                                           (8192, 320, 2880, 160, (2, 64, 64, 320)), (512, 1280, 1280, 64, None),
+                                           (384, 1152, 1152, 256, None), (2048, 640, 640, 192, None)])
+@pytest.mark.parametrize("act", [None, "geglu"])
+def test_gemm_cta_pair(cuda, M, N, K, bn, conv, act):
+    """2-SM (cta_group::2) tiles -- ragged last pair included -- equal the 1-SM
+    kernel bit for bit (same K order per output element), with the epilogues."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + N + bn)
+    x = (torch.randn(M, K if conv is None else conv[3], device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    n_out = N // 2 if act == "geglu" else N
+    r = torch.randn(M, n_out, device=cuda, generator=g).bfloat16()
+    y0 = linear(x, w, bias=b, act=act, residual=r, out_dtype=torch.float32, bn=bn, split=1, conv=conv, pair=False)
+    y1 = linear(x, w, bias=b, act=act, residual=r, out_dtype=torch.float32, bn=bn, split=1, conv=conv, pair=True)
+    assert torch.equal(y0, y1)
+    ref = _ref(x if conv is None else x, w, b, act, r, 1.0) if conv is None else None
+    if ref is not None:
+        rel = ((y1 - ref).norm() / ref.norm()).item()
+        assert rel <= 8e-3, rel

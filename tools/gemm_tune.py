@@ -1,5 +1,6 @@
-"""Measure the best (bn, split) for every GEMM shape the denoiser networks
-issue and write paper_2603_25872_b200/gemm_table.json (read by netops.pick).
+"""Measure the best (bn, split, cta_pair) for every GEMM shape the denoiser
+networks issue and write paper_2603_25872_b200/gemm_table.json (read by
+netops.pick3).
 
 Each candidate is timed inside a CUDA graph of back-to-back launches with the
 shape's own epilogue (activation, residual dtype, output dtype, implicit conv),
@@ -88,13 +89,16 @@ def tune_shape(desc, dev, reps):
     results = {}
     for bn in BNS:
         for sp in SPLITS:
-            if sp > 1 and (tiles_of(bn) * sp > 148 or kb // sp < 4):
-                continue
-            run = lambda bn=bn, sp=sp: linear(x, w, bias=bias, act=act, residual=res, out=out,   # noqa: E731
-                                              bn=bn, split=sp, conv=conv)
-            results[(bn, sp)] = time_config(run, reps)
+            for pr in (0, 1):
+                if sp > 1 and (pr or tiles_of(bn) * sp > 148 or kb // sp < 4):
+                    continue
+                if pr and M < 256:
+                    continue
+                run = lambda bn=bn, sp=sp, pr=pr: linear(x, w, bias=bias, act=act, residual=res,   # noqa: E731
+                                                         out=out, bn=bn, split=sp, conv=conv, pair=bool(pr))
+                results[(bn, sp, pr)] = time_config(run, reps)
     best = min(results, key=results.get)
-    model = pick(M, N, K, 0, 0, False) if conv is None else None
+    model = (pick(M, N, K, 0, 0, False) + (0,)) if conv is None else None
     return best, results[best], results, model
 
 
@@ -124,7 +128,8 @@ def main():
         if model in res:
             tot_best += us
             tot_model += mt
-        print(f"{key:24s} best bn={best[0]:3d} split={best[1]} {us:8.1f} us   model {model} {mt:8.1f} us",
+        print(f"{key:24s} best bn={best[0]:3d} split={best[1]} pair={best[2]} {us:8.1f} us   model {model} "
+              f"{mt:8.1f} us",
               flush=True)
     print(f"tuned {len(table)} shapes in {time.time() - t0:.0f} s; sum best {tot_best:.0f} us vs model "
           f"{tot_model:.0f} us (shapes the model covers)")

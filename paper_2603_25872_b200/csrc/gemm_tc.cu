@@ -46,7 +46,25 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   return 0.5f * x * (1.f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.7071067811865476f)); }
+// GELU with the exact-erf definition; erf from the branch-free erfc rational
+// form t exp(-z^2 + P(t)), t = 1 / (1 + z/2) (|erf error| < 1.2e-7, far below the
+// bf16 rounding of the output; libm erff costs ~3x the instructions and branches)
+__device__ __forceinline__ float gelu_erf(float x) {
+  const float u = x * 0.7071067811865476f, z = fabsf(u);
+  const float t = __fdividef(1.f, fmaf(0.5f, z, 1.f));
+  float p = fmaf(t, 0.17087277f, -0.82215223f);
+  p = fmaf(t, p, 1.48851587f);
+  p = fmaf(t, p, -1.13520398f);
+  p = fmaf(t, p, 0.27886807f);
+  p = fmaf(t, p, -0.18628806f);
+  p = fmaf(t, p, 0.09678418f);
+  p = fmaf(t, p, 0.37409196f);
+  p = fmaf(t, p, 1.00002368f);
+  p = fmaf(t, p, -1.26551223f);
+  const float r = t * __expf(fmaf(-z, z, p));         // erfc(|u|)
+  const float e = copysignf(1.f - r, u);
+  return 0.5f * x * (1.f + e);
+}
 __device__ __forceinline__ float silu(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
 
 struct EpiParams {
@@ -73,12 +91,27 @@ struct EpiParams {
 // outputs), column gate, residual.  Returns the number of outputs now in v[]
 // (32, or 16 for GEGLU; output column of v[0] = n0 or n0 / 2).  Rows >= M
 // compute garbage without touching memory (the TMA store clips them).
-__device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
+// bias of columns n0..n0+31 into registers (issued early so its latency hides
+// under the accumulator's tcgen05.ld); false when it must be read per element
+__device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, float4 (&b)[8]) {
+  if (!p.bias || n0 + 32 > N || (reinterpret_cast<uintptr_t>(p.bias + n0) & 15)) return false;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) b[q] = __ldg(reinterpret_cast<const float4*>(p.bias + n0) + q);
+  return true;
+}
+
+__device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32],
+                                          const float4 (&bpre)[8], bool have_bpre) {
   const bool row_ok = row < M;
   const bool full = n0 + 32 <= N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
-  if (p.bias) {
+  if (have_bpre) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      v[4 * q] += bpre[q].x; v[4 * q + 1] += bpre[q].y; v[4 * q + 2] += bpre[q].z; v[4 * q + 3] += bpre[q].w;
+    }
+  } else if (p.bias) {
     if (full && ((reinterpret_cast<uintptr_t>(p.bias + n0) & 15) == 0)) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -221,7 +254,8 @@ __device__ __forceinline__ void epi_store_direct(const EpiParams& p, int M, int 
 }
 
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
-  const int nout = epi_math32(p, M, N, row, n0, v);
+  float4 nob[8];
+  const int nout = epi_math32(p, M, N, row, n0, v, nob, false);
   const bool geglu = nout == 16;
   epi_store_direct(p, M, geglu ? N / 2 : N, row, geglu ? n0 / 2 : n0, nout, v);
 }
@@ -436,6 +470,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += 2) {
         const int n0 = nt * BN + c * 32;
+        float4 bpre[8];
+        const bool have_b = split == 1 && n0 < N && load_bias32(ep, N, n0, bpre);
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         tc::tmem_ld_wait();
@@ -450,7 +486,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else if (ep.tma_store) {
-          epi_math32(ep, M, N, row, n0, v);
+          epi_math32(ep, M, N, row, n0, v, bpre, have_b);
           // the buffer about to be written must have been read by its last store
           if (lane == 0) {
             if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
@@ -698,6 +734,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += 2) {
         const int n0 = nt * BN + c * 32;
+        float4 bpre[8];
+        const bool have_b = n0 < N && load_bias32(ep, N, n0, bpre);
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         tc::tmem_ld_wait();
@@ -706,7 +744,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if (ep.tma_store) {
-          epi_math32(ep, M, N, row, n0, v);
+          epi_math32(ep, M, N, row, n0, v, bpre, have_b);
           if (lane == 0) {
             if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
           }

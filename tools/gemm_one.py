@@ -1,5 +1,5 @@
 """Run one GEMM (or implicit 3x3 conv) shape a few times, for ncu captures.
-    python tools/gemm_one.py M N K [bn]          plain GEMM
+    python tools/gemm_one.py M N K [bn] [act] [res]   GEMM (act: none|geglu|gelu_tanh|silu, res: 0|1)
     python tools/gemm_one.py conv N H W C Co      implicit conv"""
 import os
 import sys
@@ -20,10 +20,15 @@ def main():
     else:
         M, N, K = (int(v) for v in sys.argv[1:4])
         bn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+        act = sys.argv[5] if len(sys.argv) > 5 and sys.argv[5] != "none" else None
+        res = len(sys.argv) > 6 and sys.argv[6] == "1"
         x = torch.randn(M, K, device=dev).bfloat16()
-        wt = torch.randn(N, K, device=dev).bfloat16()
-        out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-        run = lambda: linear(x, wt, out=out, bn=bn)   # noqa: E731
+        wt = (torch.randn(N, K, device=dev) * 0.05).bfloat16()
+        n_out = N // 2 if act == "geglu" else N
+        out = torch.empty(M, n_out, device=dev, dtype=torch.bfloat16)
+        r = torch.randn(M, n_out, device=dev).bfloat16() if res else None
+        b = torch.randn(N, device=dev)
+        run = lambda: linear(x, wt, bias=b, act=act, residual=r, out=out, bn=bn)   # noqa: E731
     for _ in range(5):
         run()
     torch.cuda.synchronize()

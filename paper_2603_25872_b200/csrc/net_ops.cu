@@ -5,6 +5,7 @@
 //   * DiT helpers: sinusoidal timestep embedding, patchify / unpatchify,
 //     SiLU->bf16 cast.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <cuda_bf16.h>
 #include <math.h>
 #include <stdint.h>
@@ -87,6 +88,62 @@ __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_
       reinterpret_cast<uint2*>(out + (int64_t)row * ldo)[c4] = u;
     }
   }
+}
+
+// Row-per-CTA LayerNorm: thread = one float4 of the row (C/4 threads), every
+// operand (x, gamma, beta, adaLN scale / shift) loaded before any arithmetic,
+// two-pass mean / variance with fixed-order block reductions (deterministic).
+// Many small CTAs instead of one warp per row: small-M rows (the 16x16 / 8x8
+// levels, DiT) no longer leave most SMs idle.
+__device__ __forceinline__ float block_sum_fixed(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(512)
+layernorm_row_kernel(const void* __restrict__ x, int64_t ldx, int x_f32, int C, const float* __restrict__ gamma,
+                     const float* __restrict__ beta, const float* __restrict__ shift, const float* __restrict__ scale,
+                     int mod_group, int64_t mod_ld, float eps, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int row = blockIdx.x, c4 = threadIdx.x;
+  const bool ok = c4 < (C >> 2);
+  const int64_t mofs = mod_group > 0 ? (int64_t)(row / mod_group) * mod_ld : 0;
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f), g = make_float4(1.f, 1.f, 1.f, 1.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 sc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) {
+    if (x_f32) {
+      v = reinterpret_cast<const float4*>(static_cast<const float*>(x) + (int64_t)row * ldx)[c4];
+    } else {
+      const uint2 u = reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(x) + (int64_t)row * ldx)[c4];
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      v = make_float4(a.x, a.y, bb.x, bb.y);
+    }
+    if (gamma) g = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
+    if (beta) b = __ldg(reinterpret_cast<const float4*>(beta) + c4);
+    if (scale) sc = __ldg(reinterpret_cast<const float4*>(scale + mofs) + c4);
+    if (shift) sh = __ldg(reinterpret_cast<const float4*>(shift + mofs) + c4);
+  }
+  const float mean = block_sum_fixed((v.x + v.y) + (v.z + v.w), red) / C;
+  const float a0 = v.x - mean, a1 = v.y - mean, a2 = v.z - mean, a3 = v.w - mean;
+  const float var = block_sum_fixed(ok ? (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3) : 0.f, red) / C;
+  const float rstd = rsqrtf(var + eps);
+  if (!ok) return;
+  float y0 = a0 * rstd * g.x + b.x, y1 = a1 * rstd * g.y + b.y, y2 = a2 * rstd * g.z + b.z, y3 = a3 * rstd * g.w + b.w;
+  if (scale) { y0 *= 1.f + sc.x; y1 *= 1.f + sc.y; y2 *= 1.f + sc.z; y3 *= 1.f + sc.w; }
+  if (shift) { y0 += sh.x; y1 += sh.y; y2 += sh.z; y3 += sh.w; }
+  uint2 u;
+  *reinterpret_cast<__nv_bfloat162*>(&u.x) = __floats2bfloat162_rn(y0, y1);
+  *reinterpret_cast<__nv_bfloat162*>(&u.y) = __floats2bfloat162_rn(y2, y3);
+  reinterpret_cast<uint2*>(out + (int64_t)row * ldo)[c4] = u;
 }
 
 // ------------------------------------------------------------ attention ---
@@ -726,10 +783,19 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
   if (!x || !out || C > 128 * 16 || C % 4 || ldx % 4 || ldo % 4 || (mod_group > 0 && mod_ld % 4)) return DRS_ERR_VALUE;
   auto mis = [](const void* p, uintptr_t a) { return p && (reinterpret_cast<uintptr_t>(p) & (a - 1)); };
   if (mis(x, x_f32 ? 16 : 8) || mis(out, 8) || mis(shift, 16) || mis(scale, 16)) return DRS_ERR_VALUE;
-  const int warps = 8;
-  dim3 grid((M + warps - 1) / warps);
   cudaStream_t st = (cudaStream_t)stream;
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
+  // measured (tools/ln_bench.py): one CTA per row wins for wide rows (C >= 1024)
+  // and for few rows (M <= 1024); one warp per row wins for narrow rows at large M
+  const bool row_path = C >= 1024 || M <= 1024;
+  if (row_path && C / 4 <= 512 && !mis(gamma, 16) && !mis(beta, 16)) {         // row-per-CTA path
+    const int thr = ((C / 4 + 31) / 32) * 32;
+    launch_pdl(layernorm_row_kernel, dim3(M), dim3(thr), 0, st, x, ldx, x_f32, C, gamma, beta, shift, scale,
+               mod_group, mod_ld, eps, o, ldo);
+    return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+  }
+  const int warps = 8;
+  dim3 grid((M + warps - 1) / warps);
   const int v4 = (C / 4 + 31) / 32;
 #define DRS_LN(K) launch_pdl(layernorm_kernel<K>, dim3(grid), dim3(warps * 32), 0, st, x, ldx, x_f32, M, C, gamma, beta, shift, scale, \
                                                                   mod_group, mod_ld, eps, o, ldo)

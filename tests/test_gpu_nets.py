@@ -172,3 +172,28 @@ def test_groupnorm(cuda, N, HW, C, G, f32, silu):
         gr.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("M,C,f32,mod", [(8192, 320, True, False), (2048, 640, False, False), (512, 1280, True, False),
+                                         (2048, 1280, True, False), (77, 1152, True, True), (4096, 1152, False, True)])
+def test_layernorm_paths(cuda, M, C, f32, mod):
+    """Both LayerNorm kernels (one warp per row for narrow rows at large M, one
+    CTA per row otherwise) vs torch fp32, with affine and adaLN modulation."""
+    from paper_2603_25872_b200.netops import layernorm
+    g = torch.Generator(device=cuda).manual_seed(M + C)
+    x = torch.randn(M, C, device=cuda, generator=g) * 3 + 1
+    x = x if f32 else x.bfloat16()
+    gamma = torch.randn(C, device=cuda, generator=g)
+    beta = torch.randn(C, device=cuda, generator=g)
+    kw = dict(gamma=gamma, beta=beta, eps=1e-5)
+    ref = torch.nn.functional.layer_norm(x.float(), (C,), gamma, beta, 1e-5)
+    if mod:
+        groups = (M + 63) // 64
+        shift = torch.randn(groups, C, device=cuda, generator=g)
+        scale = torch.randn(groups, C, device=cuda, generator=g) * 0.1
+        kw.update(shift=shift, scale=scale, mod_group=64)
+        idx = torch.arange(M, device=cuda) // 64
+        ref = ref * (1 + scale[idx]) + shift[idx]
+    y = layernorm(x, **kw)
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 3e-2 * max(1.0, ref.abs().max().item()), err

@@ -207,7 +207,7 @@ class UNet:
         return self._lin(A, wb[0], bias=wb[1], **kw), Ho, Wo
 
     # ---------------------------------------------------------------- blocks ---
-    def _resblock(self, r, x, skip, N, H, W, temb_all):
+    def _resblock(self, r, x, skip, N, H, W, temb_all, out_tag=None):
         c1, c2, co = r["c1"], r["c2"], r["co"]
         HW = H * W
         if c2:
@@ -227,11 +227,11 @@ class UNet:
             self._lin(x, r["sc"][0], bias=r["sc"][1], out=short)
         else:
             short = x
-        out = self.buf(f"res_out{co}_{HW}", (N * HW, co))
+        out = self.buf(out_tag or f"res_out{co}_{HW}", (N * HW, co))
         self._conv3(hn2, co, None, 0, N, H, W, r["conv2"], out=out, residual=short)
         return out
 
-    def _transformer(self, t, x, N, H, W):
+    def _transformer(self, t, x, N, H, W, out_tag=None):
         cfg = self.cfg
         c, HW = t["c"], H * W
         M = N * HW
@@ -246,6 +246,7 @@ class UNet:
         vt = self.buf(f"vt{c}_{HW}", (c, M))
         att = self.buf(f"att{c}_{HW}", (M, c))
         ffb = self.buf(f"ff{c}_{HW}", (M, 4 * c))
+        sb = self.buf(f"txsb{c}_{HW}", (M, c))              # bf16 copy of the stream for proj_out
         for L in t["layers"]:
             ops.layernorm(s, out=n1, gamma=L["ln1"][0], beta=L["ln1"][1], eps=1e-5)
             self._lin(n1, L["qkv"][:2 * c], out=qk)                       # Q | K
@@ -261,9 +262,8 @@ class UNet:
             ops.layernorm(s, out=n1, gamma=L["ln3"][0], beta=L["ln3"][1], eps=1e-5)
             self._lin(n1, L["ff1"][0], bias=L["ff1"][1], act="geglu", out=ffb)
             self._lin(ffb, L["ff2"][0], bias=L["ff2"][1], residual=s, out=s)
-        sb = self.buf(f"txsb{c}_{HW}", (M, c))
         ops.cast_f32_bf16(s, sb)
-        out = self.buf(f"tx_out{c}_{HW}", (M, c))
+        out = self.buf(out_tag or f"tx_out{c}_{HW}", (M, c))
         self._lin(sb, t["pout"][0], bias=t["pout"][1], residual=x, out=out)
         return out
 
@@ -305,21 +305,26 @@ class UNet:
         self._conv3(x_in, 64, None, 0, N, S, S, p["conv_in"], out=h)
         H = W = S
         cur_c = cfg.channels[0]
-        saved = [self._save(h, 0, H)]
-        for kind, blk, lev in self.blocks:
+        saved = [(h, H)]                  # h_in is written once per forward: no copy
+        blocks = self.blocks
+        for bi, (kind, blk, lev) in enumerate(blocks):
+            # a block whose output becomes a skip connection writes it straight into
+            # its own buffer (no copy out of a reused one)
+            pushed = bi + 1 < len(blocks) and blocks[bi + 1][0] == "push"
+            tag = f"skip{len(saved)}" if pushed else None
             if kind == "res":
                 skip = None
                 if blk["c2"]:
                     skip, sH = saved.pop()
                     assert sH == H, (sH, H)
-                h = self._resblock(blk, h, skip, N, H, W, temb_all)
+                h = self._resblock(blk, h, skip, N, H, W, temb_all, out_tag=tag)
                 cur_c = blk["co"]
             elif kind == "tx":
-                h = self._transformer(blk, h, N, H, W)
+                h = self._transformer(blk, h, N, H, W, out_tag=tag)
             elif kind == "push":
-                saved.append(self._save(h, len(saved), H))
+                saved.append((h, H))
             elif kind == "down":
-                out = self.buf(f"down{cur_c}_{H}", (N * (H // 2) * (W // 2), cur_c))
+                out = self.buf(tag or f"down{cur_c}_{H}", (N * (H // 2) * (W // 2), cur_c))
                 h, H, W = self._conv3(h, cur_c, None, 0, N, H, W, blk, stride=2, out=out)
             elif kind == "up":
                 out = self.buf(f"up{cur_c}_{H}", (N * 4 * H * W, cur_c))
@@ -334,8 +339,3 @@ class UNet:
         self._count = False
         return outs
 
-    def _save(self, h, i, H):
-        """Skip tensors are copied out of the producing block's (reused) output buffer."""
-        s = self.buf(f"skip{i}", tuple(h.shape))
-        s.copy_(h)
-        return s, H

@@ -9,8 +9,10 @@
 #include <cuda_bf16.h>
 #include <math.h>
 #include <stdint.h>
+#include <cuda.h>
 #include "drs_net.h"
 #include "pdl.cuh"
+#include "tc_common.cuh"
 
 namespace drs {
 
@@ -708,6 +710,149 @@ gn_cluster_kernel(const void* __restrict__ x, int HW, int C, int G, int gpc, con
   gn_stamp(4);
 }
 
+// TMA variant of the cluster GroupNorm (bf16 input): the CTA's slice (rpc rows
+// x cg*gpc channels) arrives in shared memory through a few 2-D bulk-tensor
+// loads (full-rate streaming instead of per-thread 16-byte loads), the stats,
+// cluster exchange and the in-place apply run on shared memory, and a few
+// bulk-tensor stores write the slice back.  rpc = HW / kGnCs exactly, in boxes
+// of `box` rows that divide it, so no CTA writes outside its own rows.
+__global__ void __launch_bounds__(512)
+gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int HW, int C,
+              int G, int gpc, const float* __restrict__ gamma, const float* __restrict__ beta, float eps, int silu,
+              int rpc, int box) {
+  extern __shared__ __align__(1024) uint8_t gsm_t[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_t) + 1023) & ~uintptr_t(1023));
+  const int cg = C / G, Cc = cg * gpc;
+  const int P = Cc / 8, R = blockDim.x / P;
+  const int t = threadIdx.x, q = t % P, rr = t / P;
+  const int rank = blockIdx.x % kGnCs, cl = blockIdx.x / kGnCs;
+  const int n_chunks = G / gpc;
+  const int n = cl / n_chunks, chunk = cl % n_chunks;
+  const int row0 = rank * rpc;
+  const int cbase = chunk * Cc, c0 = 8 * q;
+  const int g_lo = c0 / cg, n_lo = min(8, (g_lo + 1) * cg - c0);
+  const size_t slice_bytes = (size_t)rpc * Cc * 2;
+  uint8_t* slice = base;                                                   // [rpc][Cc] bf16
+  float4* red = reinterpret_cast<float4*>(base + ((slice_bytes + 127) & ~size_t(127)));
+  float2* csum = reinterpret_cast<float2*>(red + blockDim.x);              // [gpc]
+  float* stat = reinterpret_cast<float*>(csum + 32);                       // [gpc][2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stat + 64);
+  if (t == 0) {
+    tc::tma_prefetch(&tin);
+    tc::tma_prefetch(&tout);
+    tc::mbar_init(bar, 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  if (t == 0) {
+    tc::mbar_arrive_expect_tx(bar, (uint32_t)slice_bytes);
+    for (int k = 0; k < rpc / box; ++k)
+      tc::tma_load_2d(&tin, bar, slice + (size_t)k * box * Cc * 2, cbase, n * HW + row0 + k * box);
+  }
+  tc::mbar_wait(bar, 0);
+  float s_lo = 0.f, ss_lo = 0.f, s_hi = 0.f, ss_hi = 0.f;
+  if (rr < R) {
+    for (int r = rr; r < rpc; r += R) {
+      const uint4 u = *reinterpret_cast<const uint4*>(slice + ((size_t)r * Cc + c0) * 2);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        if (2 * e < n_lo) { s_lo += f.x; ss_lo += f.x * f.x; } else { s_hi += f.x; ss_hi += f.x * f.x; }
+        if (2 * e + 1 < n_lo) { s_lo += f.y; ss_lo += f.y * f.y; } else { s_hi += f.y; ss_hi += f.y * f.y; }
+      }
+    }
+  }
+  red[t] = make_float4(s_lo, ss_lo, s_hi, ss_hi);
+  __syncthreads();
+  for (int g = t; g < gpc; g += blockDim.x) {            // fixed order: packs, then row lanes
+    float a = 0.f, b = 0.f;
+    const int qa = (g * cg) / 8, qb = ((g + 1) * cg - 1) / 8;
+    for (int qq = qa; qq <= qb; ++qq) {
+      const bool lo = (8 * qq) / cg == g;
+      for (int r2 = 0; r2 < R; ++r2) {
+        const float4 f = red[r2 * P + qq];
+        a += lo ? f.x : f.z;
+        b += lo ? f.y : f.w;
+      }
+    }
+    csum[g] = make_float2(a, b);
+  }
+  gn_cluster_sync();
+  pdl_trigger();
+  for (int g = t; g < gpc; g += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int r2 = 0; r2 < kGnCs; ++r2) {
+      const float2 f = gn_dsmem_ld2(&csum[g], r2);
+      a += f.x;
+      b += f.y;
+    }
+    const float cnt = (float)HW * cg;
+    const float mean = a / cnt;
+    const float var = fmaxf(b / cnt - mean * mean, 0.f);
+    stat[2 * g] = mean;
+    stat[2 * g + 1] = rsqrtf(var + eps);
+  }
+  gn_cluster_sync();
+  if (rr < R) {
+    float sa[8], sb[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int g = (c0 + e) / cg;
+      sa[e] = stat[2 * g + 1] * __ldg(gamma + cbase + c0 + e);
+      sb[e] = __ldg(beta + cbase + c0 + e) - stat[2 * g] * sa[e];
+    }
+    for (int r = rr; r < rpc; r += R) {
+      uint4* p4 = reinterpret_cast<uint4*>(slice + ((size_t)r * Cc + c0) * 2);
+      uint4 u = *p4;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        float y0 = f.x * sa[2 * e] + sb[2 * e], y1 = f.y * sa[2 * e + 1] + sb[2 * e + 1];
+        if (silu) { y0 = silu_fast(y0); y1 = silu_fast(y1); }
+        h[e] = __floats2bfloat162_rn(y0, y1);
+      }
+      *p4 = u;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (t == 0) {
+    for (int k = 0; k < rpc / box; ++k) {
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                   :: "l"(&tout), "r"(tc::smem_u32(slice + (size_t)k * box * Cc * 2)), "r"(cbase),
+                      "r"(n * HW + row0 + k * box) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+typedef CUresult (*PFN_encodeTiledGn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool gn_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int C, int box_c, int box_r) {
+  static PFN_encodeTiledGn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<PFN_encodeTiledGn>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)C * 2};
+  cuuint32_t boxd[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, boxd, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int gn_num_sms() {
   static int n = 0;
   if (!n) {
@@ -722,12 +867,12 @@ static int gn_num_sms() {
 // per cluster: the smallest divisor of G whose channel span is a multiple of
 // 8 and that still leaves >= ~#SMs CTAs, so small batches fill the GPU.
 static bool gn_cluster_plan(int N, int HW, int C, int G, int x_f32, int& gpc, int& rpc, int& threads, int& keep,
-                            size_t& smem) {
+                            size_t& smem, bool size_cap = true) {
   const int cg = C / G;
   if (C % 8 || cg < 8 || G > 32) return false;
   // measured (tools/gn_bench.py): the cluster path wins up to ~12 MB of input;
   // beyond that the two-kernel path's wider grid streams faster
-  if ((int64_t)N * HW * C * (x_f32 ? 4 : 2) > 12 * 1024 * 1024) return false;
+  if (size_cap && (int64_t)N * HW * C * (x_f32 ? 4 : 2) > 12 * 1024 * 1024) return false;
   gpc = 0;
   for (int d = 1; d <= G; ++d) {
     if (G % d || (cg * d) % 8 || (cg * d) / 8 > 512) continue;
@@ -888,8 +1033,44 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
   cudaStream_t st = (cudaStream_t)stream;
   int gpc, rpc, threads, keep;
   size_t smem;
-  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
-      gn_cluster_plan(N, HW, C, G, x_f32, gpc, rpc, threads, keep, smem)) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (aligned && !x_f32 && HW % kGnCs == 0 && gn_cluster_plan(N, HW, C, G, 0, gpc, rpc, threads, keep, smem) &&
+      rpc == HW / kGnCs) {
+    // TMA slice path: boxes of `box` rows dividing rpc, slice (+ scratch) within 200 KB
+    int box = rpc < 256 ? rpc : 256;
+    while (box > 1 && rpc % box) --box;
+    const int Cc = (C / G) * gpc;
+    const size_t slice = (size_t)rpc * Cc * 2;
+    const size_t need = ((slice + 127) & ~size_t(127)) + (size_t)threads * 16 + 32 * 8 + 64 * 4 + 64 + 1024;
+    CUtensorMap tin, tout;
+    if (box >= 8 && need <= 200 * 1024 && gn_tmap(&tin, x, (int64_t)N * HW, C, Cc, box) &&
+        gn_tmap(&tout, out, (int64_t)N * HW, C, Cc, box)) {
+      static bool attr = false;
+      if (!attr) {
+        if (cudaFuncSetAttribute(gn_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+            cudaSuccess)
+          return DRS_ERR_CUDA;
+        attr = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(N * (G / gpc) * kGnCs);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = need;
+      cfg.stream = st;
+      cudaLaunchAttribute la[2];
+      la[0].id = cudaLaunchAttributeClusterDimension;
+      la[0].val.clusterDim.x = kGnCs;
+      la[0].val.clusterDim.y = 1;
+      la[0].val.clusterDim.z = 1;
+      la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      la[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = la;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
+      cudaLaunchKernelEx(&cfg, gn_tma_kernel, tin, tout, HW, C, G, gpc, gamma, beta, eps, silu, rpc, box);
+      return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+    }
+  }
+  if (aligned && gn_cluster_plan(N, HW, C, G, x_f32, gpc, rpc, threads, keep, smem)) {
     auto kern = x_f32 ? gn_cluster_kernel<true> : gn_cluster_kernel<false>;
     static bool attr[2] = {false, false};
     if (!attr[x_f32 ? 1 : 0]) {

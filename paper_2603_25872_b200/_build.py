@@ -53,7 +53,7 @@ def _deps():
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     newest_dep = max(os.path.getmtime(p) for p in _deps())
-    objs = []
+    objs, cmds = [], []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)
         if not os.path.exists(s):
@@ -62,10 +62,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if not force and os.path.exists(o) and os.path.getmtime(o) >= newest_dep:
             continue
-        cmd = [nvcc()] + _flags() + extra + ["-c", s, "-o", o]
+        cmds.append([nvcc()] + _flags() + extra + ["-c", s, "-o", o])
+    # translation units compile in parallel (the GEMM / attention TUs dominate)
+    procs = []
+    for cmd in cmds:
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
         if verbose:

@@ -29,17 +29,26 @@ SHAPES = [
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--only", default="", help="substring of the shape label to run")
+    ap.add_argument("--eager", type=int, default=0, help="N eager launches only (for ncu), no timing")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import netops
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     for label, B, H, Lq, Lk, d in SHAPES:
+        if a.only and a.only not in label:
+            continue
         vt_img = (Lk + 7) // 8 * 8
         q = torch.randn(B * Lq, H * d, device=dev, generator=g).bfloat16()
         k = torch.randn(B * Lk, H * d, device=dev, generator=g).bfloat16()
         vt = torch.randn(H * d, B * vt_img, device=dev, generator=g).bfloat16()
         o = torch.empty(B * Lq, H * d, device=dev, dtype=torch.bfloat16)
+        if a.eager:
+            for _ in range(a.eager):
+                netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)
+            torch.cuda.synchronize()
+            continue
         s = torch.cuda.Stream(dev)
         with torch.cuda.stream(s):
             netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)

@@ -391,8 +391,11 @@ def main():
                     "algo_bytes_per_launch": algo, "avg_launch_us": avg_ms * 1e3,
                     "peak_source": "fallback" if peaks.get("_fallback") else "MEASURED_PEAKS.json hbm_gbs"}
     prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(prof) and not net_cfg:
-        roofline["traffic"] = json.load(open(prof)).get(roofline["kernel"])
+    if os.path.exists(prof):
+        tr = json.load(open(prof))
+        roofline["traffic"] = tr.get(roofline["kernel"])
+        if roofline["traffic"] is not None and net_cfg:
+            roofline["traffic_detail"] = tr.get("_detail")
 
     # draft-and-refine on this one GPU (logical devices batched per round), for context
     drf = {"T": cfg["T"], "mode_timed": mode, "devices": n}

@@ -309,7 +309,6 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem,
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Implicit-GEMM 3x3 convolution (stride 1, pad 1) over an NHWC bf16 input:
 // A[(n,y,x), (ky,kx,c)] is never materialised -- the k-block (tap, 64-channel
@@ -509,7 +508,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty_bar[acc]);
     }
-    if (ep.tma_store && lane == 0) bulk_wait_all();
+    if (ep.tma_store && lane == 0) bulk_wait_read<0>();   // smem reads done; the writes complete with the grid
   }
   if (split > 1) {
     // ---------------- cluster split-K reduction over DSMEM ----------------
@@ -766,7 +765,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
     }
-    if (ep.tma_store && lane == 0) bulk_wait_all();
+    if (ep.tma_store && lane == 0) bulk_wait_read<0>();   // smem reads done; the writes complete with the grid
   }
   __syncwarp();
   tc::tc_fence_before();

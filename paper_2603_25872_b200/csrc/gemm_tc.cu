@@ -776,6 +776,171 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
   }
 }
 
+// ---- CTA pair + cluster split-K: small-M, long-K GEMMs ----
+// A cluster of 2 * split CTAs owns one 256 x BN output tile: ranks (2s, 2s+1)
+// are a tcgen05 CTA pair (as in gemm_pair_kernel: each CTA its 128 A rows and
+// half of the B tile) accumulating K range s; the pairs then park their fp32
+// partial tiles in their own (idle) pipeline smem and, after one cluster
+// barrier, CTA (h, s) reduces rows s, s + split, ... of half h over the split
+// peers (ranks h, h + 2, ...) through DSMEM in the fixed order 0..split-1
+// (deterministic, no workspace) and runs the epilogue.  Operand ingest per SM
+// per k-block is (128 + BN/2) x 128 B -- the pair kernel's -- while split-K
+// keeps every SM busy on the few tiles of a small-M layer.
+__device__ __forceinline__ void mma_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(tc::smem_u32(bar)), "h"(mask) : "memory");
+}
+
+template <int BN, int kStages>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       int M, int N, int K, int split, EpiParams ep, ConvGeom cv) {
+  using S = PairSmem<BN, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;       // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull_bar + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)pair_rank();               // rank in the 2 * split cluster
+  const int half = rank & 1, sp = rank >> 1;
+  const uint16_t pair_mask = (uint16_t)(3u << (rank & ~1));
+  const int pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
+  const int tile = blockIdx.x / (2 * split);
+  const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
+  const int m0 = (pmt * 2 + half) * kBM;
+  const int num_kb = (K + kBK - 1) / kBK;
+  const int kb_per = (num_kb + split - 1) / split;
+  const int kb0 = sp * kb_per, kb1 = min(num_kb, kb0 + kb_per);
+  constexpr uint32_t kTmemCols = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
+  constexpr uint32_t kIdesc = tc::idesc_bf16_f32(2 * kBM, BN);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmap_a);
+    tc::tma_prefetch(&tmap_b);
+    for (int s2 = 0; s2 < kStages; ++s2) { tc::mbar_init(&full_bar[s2], 1); tc::mbar_init(&empty_bar[s2], 1); }
+    tc::mbar_init(&tfull_bar[0], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(tc::smem_u32(tmem_slot)), "n"(kTmemCols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  pair_sync();                                      // barriers and TMEM of the whole cluster are ready
+  tc::tc_fence_after();
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * S::kStageBytes;
+        uint8_t* sb = sa + S::kABytes;
+        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+        if (cv.on) {
+          const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
+          const int ky = tap / 3, kx = tap - ky * 3;
+          const int hw = cv.H * cv.W;
+          const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+          tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+        } else {
+          tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
+        }
+        tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + half * (BN / 2));
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (half == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full_bar[stage], phase);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint8_t* sa = smem + stage * S::kStageBytes;
+          const uint64_t da = tc::smem_desc_sw128(sa);
+          const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16_pair(tmem_base, da + 2 * k, db + 2 * k, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          mma_commit_pair_mask(&empty_bar[stage], pair_mask);
+          if (kb == kb1 - 1) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
+        if (tc::elect_one()) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
+        __syncwarp();
+      }
+    }
+  } else {
+    // partial tile (this CTA's 128 rows) -> own smem, padded rows
+    const int quad = warp & 3;
+    const int hw_ = (warp - 2) >> 2;
+    tc::mbar_wait(&tfull_bar[0], 0);
+    tc::tc_fence_after();
+#pragma unroll 1
+    for (int c = hw_; c < BN / 32; c += 2) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + c * 32, r);
+      tc::tmem_ld_wait();
+      float* dst = reinterpret_cast<float*>(smem) + (quad * 32 + lane) * (BN + 4) + c * 32;
+      const bool z = kb1 <= kb0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(dst + 4 * q) =
+            z ? make_float4(0.f, 0.f, 0.f, 0.f)
+              : make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                            __uint_as_float(r[4 * q + 3]));
+    }
+  }
+  __syncwarp();
+  tc::tc_fence_before();
+  cluster_sync();                                  // every partial tile of the cluster is in smem
+  if (warp >= 2) {
+    const int t = threadIdx.x - 64;                // 0..255
+    const uint32_t base = tc::smem_u32(smem);
+    constexpr int kChunks = BN / 32;
+    const int rows_here = (kBM - sp + split - 1) / split;      // rows sp, sp + split, ...
+    for (int item = t; item < rows_here * kChunks; item += kEpiWarps * 32) {
+      const int r = sp + (item / kChunks) * split;
+      const int c = item % kChunks;
+      const int n0 = nt * BN + c * 32;
+      if (n0 >= N) continue;
+      const uint32_t off = (uint32_t)((r * (BN + 4) + c * 32) * 4);
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      for (int s2 = 0; s2 < split; ++s2) {
+        const uint32_t ra = dsmem_map(base + off, half + 2 * s2);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 f = dsmem_ld4(ra + 16 * q);
+          v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+        }
+      }
+      epilogue32(ep, M, N, m0 + r, n0, v);
+    }
+  }
+  __syncwarp();
+  cluster_sync();                                  // peers are done reading this CTA's smem
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "n"(kTmemCols) : "memory");
+  }
+}
+
 // ------------------------------------------------------------ host side ---
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -964,6 +1129,39 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+
+template <int BN, int kStages>
+static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
+                             const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
+  using S = PairSmem<BN, kStages>;
+  static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "pair split-K partial tile must fit the ring");
+  auto kern = gemm_pair_split_kernel<BN, kStages>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return DRS_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles * 2 * split);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = S::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeClusterDimension;
+  la[0].val.clusterDim.x = 2 * split;
+  la[0].val.clusterDim.y = 1;
+  la[0].val.clusterDim.z = 1;
+  la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, split, ep, cv);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
 static int max_clusters_bn(int bn, int split) {
   switch (bn) {
     case 64: return max_clusters<64, 8>(split);
@@ -1062,8 +1260,8 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
     return DRS_ERR_CUDA;
   }
-  // 2-SM pair mode: M >= 256, no split-K
-  const bool pair = g->cta_pair > 0 && split == 1 && M >= 2 * kBM;
+  // 2-SM pair mode: M >= 256 (split > 1: pair + cluster split-K, 2 * split <= 16 CTAs)
+  const bool pair = g->cta_pair > 0 && M >= 2 * kBM;
   if (!make_tmap(&tb, g->B, N, K, g->ldb, pair ? bn / 2 : bn)) return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0};
@@ -1079,6 +1277,14 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
+  if (pair && split > 1) {
+    ep.tma_store = 0;                              // reduced rows are stored directly
+    if (bn == 64) return launch_pair_split<64, 8>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 128) return launch_pair_split<128, 8>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 160) return launch_pair_split<160, 7>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 192) return launch_pair_split<192, 6>(ta, tb, M, N, K, split, ep, cv, st);
+    return launch_pair_split<256, 6>(ta, tb, M, N, K, split, ep, cv, st);
+  }
   if (pair) {
     if (bn == 64) return launch_pair<64, 8>(ta, tb, tcm, M, N, K, ep, cv, st);
     if (bn == 128) return launch_pair<128, 8>(ta, tb, tcm, M, N, K, ep, cv, st);

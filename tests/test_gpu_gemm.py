@@ -142,3 +142,28 @@ def test_gemm_cta_pair(cuda, M, N, K, bn, conv, act):
     if ref is not None:
         rel = ((y1 - ref).norm() / ref.norm()).item()
         assert rel <= 8e-3, rel
+
+
+@pytest.mark.parametrize("M,N,K,bn,conv,split", [(512, 1280, 11520, 128, None, 3), (512, 1280, 1280, 64, None, 2),
+                                                 (300, 256, 1152, 256, None, 4), (512, 256, 192, 128, None, 4),
+                                                 (512, 1280, 11520, 128, (2, 16, 16, 1280), 3),
+                                                 (512, 640, 5760, 64, None, 8), (1024, 320, 2880, 160, None, 6),
+                                                 (640, 192, 640, 192, None, 2)])
+def test_gemm_cta_pair_splitk(cuda, M, N, K, bn, conv, split):
+    """CTA pair + cluster split-K (2 * split CTAs per tile, DSMEM reduction in
+    split order) equals the 1-SM cluster split-K bit for bit; empty K ranges
+    (split > k-blocks) and ragged last pairs included."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + N + K + split)
+    x = (torch.randn(M, K if conv is None else conv[3], device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    r = torch.randn(M, N, device=cuda, generator=g).bfloat16()
+    y0 = linear(x, w, bias=b, residual=r, out_dtype=torch.float32, bn=bn, split=split, conv=conv, pair=False)
+    y1 = linear(x, w, bias=b, residual=r, out_dtype=torch.float32, bn=bn, split=split, conv=conv, pair=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    if conv is None:
+        ref = _ref(x, w, b, None, r, 1.0)
+        rel = ((y1 - ref).norm() / ref.norm()).item()
+        assert rel <= 8e-3, rel

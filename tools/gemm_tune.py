@@ -99,9 +99,11 @@ def tune_shape(desc, dev, reps, cold=False):
     for bn in BNS:
         for sp in SPLITS:
             for pr in (0, 1):
-                if sp > 1 and (pr or tiles_of(bn) * sp > 148 or kb // sp < 4):
-                    continue
                 if pr and M < 256:
+                    continue
+                # split-K runs one wave of clusters: 1-SM tiles x split, or pair tiles x 2 x split CTAs
+                ctas = (((M + 255) // 256) * ((N + bn - 1) // bn) * 2 if pr else tiles_of(bn)) * sp
+                if sp > 1 and (ctas > 148 or kb // sp < 4):
                     continue
                 run = lambda bn=bn, sp=sp, pr=pr: linear(x, wnext(), bias=bias, act=act, residual=res,   # noqa: E731
                                                          out=out, bn=bn, split=sp, conv=conv, pair=bool(pr))

@@ -22,6 +22,10 @@ extern "C" {
 #define DRS_ACT_SILU 2
 #define DRS_ACT_GELU_ERF 3
 #define DRS_ACT_GEGLU 4       /* weight rows interleaved (value, gate): out[n/2] = v * gelu(g) */
+#define DRS_ACT_HEADSOFTMAX 5 /* scores -> probabilities: every 96-column block (one attention head)
+                               * is softmax-normalised over its first hs_valid columns (exp2 of
+                               * the raw accumulator: fold scale * log2(e) into B), zeros after;
+                               * bf16 out, bn = 192, split = 1, one CTA per tile                */
 
 /* C[M,N] = act(alpha * A[M,K] . B[N,K]^T + bias[N]) (+ residual[M,N]).
  * A, B bf16 K-major (lda/ldb in elements, multiples of 8, 16-byte aligned),
@@ -61,6 +65,13 @@ typedef struct drs_gemm_args {
    * of operand ingest per SM per k-block instead of (128 + bn) x 128 B).
    * Needs M >= 256 and split == 1; otherwise ignored.  0: one CTA per tile. */
   int cta_pair;
+  /* Per-image B operand (CFG: unconditional / conditional context): when
+   * b_img_rows > 0, rows [m, m+128) of A with (m / b_img_rows) odd use B rows
+   * offset by b_img_off (B holds N + b_img_off rows).  b_img_rows % 128 == 0
+   * (% 256 for CTA pairs, else the pair flag is ignored). */
+  int b_img_rows, b_img_off;
+  /* DRS_ACT_HEADSOFTMAX: valid columns per 96-column head block (<= 96). */
+  int hs_valid;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
 

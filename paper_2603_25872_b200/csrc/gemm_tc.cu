@@ -84,6 +84,7 @@ struct EpiParams {
   int act;                  // DRS_ACT_*
   int out_f32;              // 1: fp32 output, 0: bf16
   int tma_store;            // 1: output written through smem staging + TMA (tmap_c)
+  int hs_valid;             // DRS_ACT_HEADSOFTMAX: valid columns per 96-column head
 };
 
 // Epilogue math on 32 consecutive accumulator columns n0..n0+31 of `row`:
@@ -319,7 +320,13 @@ struct ConvGeom {
   int on;          // 0: plain GEMM (2-D A map)
   int cblocks;     // Cin / 64
   int H, W;        // image size (W <= 128, W * rows * imgs == 128 pixels per tile)
+  int b_img_rows;  // > 0: tiles whose first row m has (m / b_img_rows) odd read B rows + b_img_off
+  int b_img_off;
 };
+
+__device__ __forceinline__ int b_row_offset(const ConvGeom& cv, int m0) {
+  return cv.b_img_rows > 0 ? ((m0 / cv.b_img_rows) & 1) * cv.b_img_off : 0;
+}
 
 __device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3) {
@@ -328,6 +335,51 @@ __device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, voi
       " [%0], [%1, {%3, %4, %5, %6}], [%2];"
       :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+
+// DRS_ACT_HEADSOFTMAX epilogue of one row: the 96 accumulator columns of one
+// head (3 TMEM chunks starting at tm_col) -> p_j = 2^(s_j - max) / sum over the
+// first `valid` columns, zeros after -> 96 bf16 at out[row, col0 ..].
+__device__ __forceinline__ void head_softmax_row(const EpiParams& ep, int M, int N, int row, int col0,
+                                                 uint32_t tm_col) {
+  uint32_t r[3][32];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) tc::tmem_ld32(tm_col + c * 32, r[c]);
+  tc::tmem_ld_wait();
+  if (row >= M || col0 >= N) return;
+  const int valid = ep.hs_valid;
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (c * 32 + e < valid) mx = fmaxf(mx, __uint_as_float(r[c][e]));
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      float pv = 0.f;
+      if (c * 32 + e < valid) {
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(pv) : "f"(__uint_as_float(r[c][e]) - mx));
+      }
+      sum += pv;
+      r[c][e] = __float_as_uint(pv);
+    }
+  const float inv = 1.f / sum;
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.out) + (int64_t)row * ep.ldo + col0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h[e] = __floats2bfloat162_rn(__uint_as_float(r[c][8 * q + 2 * e]) * inv,
+                                     __uint_as_float(r[c][8 * q + 2 * e + 1]) * inv);
+      *reinterpret_cast<uint4*>(dst + c * 32 + 8 * q) = u;
+    }
 }
 
 constexpr int kStgBytes = 4096;        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
@@ -406,7 +458,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           } else {
             tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
           }
-          tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN);
+          tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -466,6 +518,16 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const int row = mt * kBM + quad * 32 + lane;
+      if constexpr (BN == 192) {
+        if (ep.act == DRS_ACT_HEADSOFTMAX) {       // warp half h: head 2 nt + h = columns [96 h, 96 h + 96)
+          head_softmax_row(ep, M, N, row, nt * BN + half * 96,
+                           tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 96);
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty_bar[acc]);
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += 2) {
         const int n0 = nt * BN + c * 32;
@@ -679,7 +741,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
           } else {
             tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
           }
-          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + rank * (BN / 2));
+          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
+                           nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -855,7 +918,8 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         } else {
           tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
         }
-        tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + half * (BN / 2));
+        tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
+                         nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
@@ -1248,7 +1312,16 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (split < 0 || split > 8) return DRS_ERR_VALUE;            // portable cluster size
   if (bn == 0 || split == 0) gemm_auto_config(M, N, K, bn, split);
   CUtensorMap ta, tb;
-  ConvGeom cv{0, 0, 0, 0};
+  ConvGeom cv{0, 0, 0, 0, 0, 0};
+  const bool hsm = g->act == DRS_ACT_HEADSOFTMAX;
+  if (hsm) {
+    if (g->out_f32 || N % 96 || g->hs_valid <= 0 || g->hs_valid > 96 || (g->ldc % 8) ||
+        (reinterpret_cast<uintptr_t>(g->C) & 15) || g->residual || g->bias || g->colscale || g->rowbias)
+      return DRS_ERR_VALUE;
+    bn = 192;
+    split = 1;
+  }
+  if (g->b_img_rows > 0 && (g->b_img_rows % kBM || g->b_img_off <= 0)) return DRS_ERR_VALUE;
   if (g->conv_C > 0) {      // implicit 3x3 conv: A = NHWC input, M = N*H*W, K = 9*C
     const int C = g->conv_C, H = g->conv_H, W = g->conv_W, Nimg = g->conv_N;
     if (C % 64 || W > 128 || (W & (W - 1)) || (int64_t)Nimg * H * W != M || K != 9 * C) return DRS_ERR_VALUE;
@@ -1256,22 +1329,27 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
     if (W * rows * (128 / (W * rows)) != 128 || H % rows || (128 / (W * rows) > 1 && (rows != H || Nimg % (128 / (W * H)))))
       return DRS_ERR_VALUE;
     if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C)) return DRS_ERR_CUDA;
-    cv = ConvGeom{1, C / 64, H, W};
+    cv = ConvGeom{1, C / 64, H, W, 0, 0};
   } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
     return DRS_ERR_CUDA;
   }
   // 2-SM pair mode: M >= 256 (split > 1: pair + cluster split-K, 2 * split <= 16 CTAs)
-  const bool pair = g->cta_pair > 0 && M >= 2 * kBM;
-  if (!make_tmap(&tb, g->B, N, K, g->ldb, pair ? bn / 2 : bn)) return DRS_ERR_CUDA;
+  const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM));
+  if (g->b_img_rows > 0) {
+    cv.b_img_rows = g->b_img_rows;
+    cv.b_img_off = g->b_img_off;
+  }
+  if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
+    return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   CUtensorMap tcm;
   memset(&tcm, 0, sizeof(tcm));
   {
     const int elem = g->out_f32 ? 4 : 2;
     const int n_out = g->act == DRS_ACT_GEGLU ? N / 2 : N;
-    const bool ok = split == 1 && !(reinterpret_cast<uintptr_t>(g->C) & 15) && ((g->ldc * elem) % 16) == 0 &&
+    const bool ok = split == 1 && !hsm && !(reinterpret_cast<uintptr_t>(g->C) & 15) && ((g->ldc * elem) % 16) == 0 &&
                     g->ldc >= n_out;
     if (ok && make_tmap_out(&tcm, g->C, M, n_out, g->ldc, elem, g->act == DRS_ACT_GEGLU ? 16 : 32)) ep.tma_store = 1;
   }

@@ -12,7 +12,7 @@ import torch
 
 from . import _lib
 
-ACT = {None: 0, "none": 0, "gelu_tanh": 1, "silu": 2, "gelu": 3, "geglu": 4}
+ACT = {None: 0, "none": 0, "gelu_tanh": 1, "silu": 2, "gelu": 3, "geglu": 4, "headsoftmax": 5}
 
 
 # Instrumentation (bench.py): when TIMERS is a list, every GEMM records
@@ -25,17 +25,21 @@ def _ptr(t):
 
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
-           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None):
+           bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None,
+           b_img=None, hs_valid=0):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
-    rowbias (n_groups, >=N) views indexed by row // group."""
+    rowbias (n_groups, >=N) views indexed by row // group.  b_img = (rows, off): rows
+    of images with odd index (row // rows) use w[off + n] instead of w[n] (w holds
+    N + off rows; CFG pairs with per-context weights).  act="headsoftmax": per
+    96-column head, softmax (exp2) over the first hs_valid columns."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
     if conv is not None:          # implicit 3x3 conv: x is NHWC (N*H*W, C), K = 9*C
         cn, ch, cw, cc = conv
         M, K = cn * ch * cw, 9 * cc
     else:
         M, K = x.shape
-    N = w.shape[0]
+    N = w.shape[0] if b_img is None else w.shape[0] - b_img[1]
     assert w.shape[1] == K and x.stride(-1) == 1 and w.stride(1) == 1
     n_out = N // 2 if act == "geglu" else N
     if out is None:
@@ -70,6 +74,9 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     g.cta_pair = 1 if pair else 0
     if conv is not None:
         g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
+    if b_img is not None:
+        g.b_img_rows, g.b_img_off = b_img
+    g.hs_valid = hs_valid
     if GEMM_RECORD is not None:
         GEMM_RECORD.append((2.0 * M * N * K, _lib.DrsGemmArgs.from_buffer_copy(g)))
     if TIMERS is not None:

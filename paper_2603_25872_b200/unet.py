@@ -17,6 +17,7 @@ LN GEGLU FF] -> proj_out + residual), Downsample2D (conv3x3 stride 2),
 Upsample2D (nearest 2x + conv3x3).
 """
 
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -79,6 +80,8 @@ class UNet:
         self.max_batch = max_batch                   # images per forward (each is a CFG pair)
         self.latent_numel = cfg.in_ch * cfg.size * cfg.size
         self.ctx_pad = (cfg.ctx_len + 7) // 8 * 8
+        # cross-attention folded into two GEMMs against the fixed context (DRS_FOLD_CROSS=0: attention kernel)
+        self.fold_cross = os.environ.get("DRS_FOLD_CROSS", "1") != "0"
         I = _Init(self.device, seed)
         c0, T = cfg.channels[0], cfg.temb_dim
         self.p = p = {}
@@ -166,7 +169,39 @@ class UNet:
                                q2=I.mat(c, c), wk=wk, wv=wv, k_ctx=k_ctx, vt_ctx=vt_ctx,
                                o2=(I.mat(c, c), I.vec(c)), ln3=I.gn(c),
                                ff1=(I.mat(8 * c, c), I.vec(8 * c)), ff2=(I.mat(c, 4 * c), I.vec(c))))
+            if self.device.type == "cuda":
+                L = layers[-1]
+                L["ws"], L["wpv"] = self._cross_fold(L["q2"], L["o2"][0], k_ctx, vt, c)
         return dict(c=c, gn=I.gn(c), pin=(I.mat(c, c), I.vec(c)), layers=layers, pout=(I.mat(c, c), I.vec(c)))
+
+    XH = 96       # padded head width of the folded cross-attention (ctx_len <= 96)
+
+    def _cross_fold(self, wq, wo, k_ctx, vt, c):
+        """Cross-attention against the FIXED text context folded into two GEMMs:
+        S_h = (n1 Wq_h^T) K_h^T * scale = n1 (K_h Wq_h * scale)^T, so the score
+        block of head h is a GEMM with B_S[h*96 + j] = scale * log2(e) * K_h[j] Wq_h
+        (zero rows for j >= ctx_len); and sum_h P_h V_h Wo_h^T = P B_PV^T with
+        B_PV[:, h*96 + j] = Wo_h V_h[j].  One matrix per CFG context (uncond /
+        cond), stacked: image n uses context n % 2 (drs_gemm b_img).  Built once
+        in fp32 from the bf16 weights and context projections, rounded to bf16."""
+        cfg = self.cfg
+        heads = cfg.n_heads(c)
+        d = c // heads
+        T, XH = cfg.ctx_len, self.XH
+        assert T <= XH
+        f = (d ** -0.5) * 1.4426950408889634
+        wqf, wof = wq.float(), wo.float()
+        ws = torch.zeros(2, heads * XH, c, device=self.device)
+        wpv = torch.zeros(2, c, heads * XH, device=self.device)
+        for ctx in range(2):
+            K = k_ctx[ctx * T:(ctx + 1) * T].float()                    # (T, c)
+            V = vt[:, ctx * T:(ctx + 1) * T].float().t()                # (T, c)
+            for h in range(heads):
+                sl = slice(h * d, (h + 1) * d)
+                ws[ctx, h * XH:h * XH + T] = f * (K[:, sl] @ wqf[sl, :])
+                wpv[ctx, :, h * XH:h * XH + T] = wof[:, sl] @ V[:, sl].t()
+        return (ws.reshape(2 * heads * XH, c).bfloat16().contiguous(),
+                wpv.reshape(2 * c, heads * XH).bfloat16().contiguous())
 
     # --------------------------------------------------------------- buffers ---
     def buf(self, tag, shape, dtype=torch.bfloat16):
@@ -254,11 +289,21 @@ class UNet:
             self._attn(qk[:, :c], qk[:, c:], vt, att, N, heads, HW, HW, d, HW)
             self._lin(att, L["o1"][0], bias=L["o1"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln2"][0], beta=L["ln2"][1], eps=1e-5)
-            q = qk[:, :c]
-            self._lin(n1, L["q2"], out=q)
-            # every image n attends to context n % 2 (uncond / cond): one launch
-            self._attn(q, L["k_ctx"], L["vt_ctx"], att, N, heads, HW, cfg.ctx_len, d, self.ctx_pad)
-            self._lin(att, L["o2"][0], bias=L["o2"][1], residual=s, out=s)
+            if "ws" in L and HW % 128 == 0 and self.fold_cross:
+                # cross-attention folded into two GEMMs (see _cross_fold): scores ->
+                # per-head softmax in the epilogue -> P; P B_PV^T + bias + residual
+                if self._count:           # the architecture's FLOPs (q2, attention, o2), not the fold's
+                    self.flops += 2.0 * M * c * c * 2 + 4.0 * N * heads * HW * cfg.ctx_len * d
+                xh = heads * self.XH
+                pbuf = self.buf(f"xp{c}_{HW}", (M, xh))
+                ops.linear(n1, L["ws"], act="headsoftmax", hs_valid=cfg.ctx_len, b_img=(HW, xh), out=pbuf)
+                ops.linear(pbuf, L["wpv"], bias=L["o2"][1], residual=s, out=s, b_img=(HW, c))
+            else:
+                q = qk[:, :c]
+                self._lin(n1, L["q2"], out=q)
+                # every image n attends to context n % 2 (uncond / cond): one launch
+                self._attn(q, L["k_ctx"], L["vt_ctx"], att, N, heads, HW, cfg.ctx_len, d, self.ctx_pad)
+                self._lin(att, L["o2"][0], bias=L["o2"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln3"][0], beta=L["ln3"][1], eps=1e-5)
             self._lin(n1, L["ff1"][0], bias=L["ff1"][1], act="geglu", out=ffb)
             self._lin(ffb, L["ff2"][0], bias=L["ff2"][1], residual=s, out=s)

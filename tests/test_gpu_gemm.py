@@ -167,3 +167,39 @@ def test_gemm_cta_pair_splitk(cuda, M, N, K, bn, conv, split):
         ref = _ref(x, w, b, None, r, 1.0)
         rel = ((y1 - ref).norm() / ref.norm()).item()
         assert rel <= 8e-3, rel
+
+
+@pytest.mark.parametrize("M,N,K,img,bn,split,pair", [(512, 320, 640, 256, 64, 1, False), (512, 320, 640, 256, 128, 1, True),
+                                                     (1024, 768, 320, 512, 192, 1, False),
+                                                     (512, 1280, 1280, 256, 128, 2, False),
+                                                     (512, 1280, 1280, 256, 64, 2, True), (384, 256, 128, 128, 64, 1, True)])
+def test_gemm_per_image_b(cuda, M, N, K, img, bn, split, pair):
+    """b_img: rows of odd images read the second half of the B operand (the
+    CFG pair's per-context weights), in every kernel variant."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(2 * N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    y = linear(x, w, bias=b, out_dtype=torch.float32, bn=bn, split=split, pair=pair, b_img=(img, N))
+    odd = (torch.arange(M, device=cuda) // img) % 2 == 1
+    ref = torch.where(odd[:, None], _ref(x, w[N:], b, None, None, 1.0), _ref(x, w[:N], b, None, None, 1.0))
+    err = (y - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M,heads,K,valid", [(8192, 8, 320, 77), (512, 8, 1280, 77), (300, 3, 64, 96), (256, 1, 128, 5)])
+def test_gemm_head_softmax(cuda, M, heads, K, valid):
+    """act="headsoftmax": every 96-column block is exp2-softmax-normalised over
+    its first `valid` columns (zeros after), bf16 out."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + heads)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(heads * 96, K, device=cuda, generator=g) * 0.2).bfloat16()
+    y = linear(x, w, act="headsoftmax", hs_valid=valid)
+    s = (x.float() @ w.float().t()).view(M, heads, 96)
+    p = torch.zeros_like(s)
+    p[:, :, :valid] = torch.softmax(s[:, :, :valid] * 0.6931471805599453, dim=-1)
+    err = (y.float().view(M, heads, 96) - p).abs().max().item()
+    assert err <= 4e-3, err
+    assert torch.all(y.view(M, heads, 96)[:, :, valid:] == 0)

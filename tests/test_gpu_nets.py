@@ -197,3 +197,27 @@ def test_layernorm_paths(cuda, M, C, f32, mod):
     y = layernorm(x, **kw)
     err = (y.float() - ref).abs().max().item()
     assert err <= 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("size,B", [(32, 2), (32, 3)])
+@pytest.mark.parametrize("g", [0.0, 1.0])
+def test_sd15_cross_attention_fold_batched(cuda, size, B, g):
+    """Folded cross-attention (score GEMM + per-head softmax epilogue, then
+    P x (Wo V)) with per-context weights chosen by image parity, for a batch
+    of CFG pairs: every image vs the fp32 torch reference (rel-L2 <= 3e-2, as
+    the B = 1 test), and the attention-kernel path on the same net likewise."""
+    from paper_2603_25872_b200.unet import UNet, sd15_config
+    from nets_ref import unet_ref
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    net = UNet(sd15_config(size), cuda, seed=0, max_batch=B, cfg_scale=g)
+    x = torch.randn(B, 4, size, size, device=cuda, dtype=torch.float64)
+    t = torch.tensor([601.0, 233.0, 901.0][:B], device=cuda)
+    ref = unet_ref(net, x.float(), t)
+    for fold in (True, False):
+        net.fold_cross = fold
+        o = [torch.empty(4 * size * size, device=cuda) for _ in range(B)]
+        net.forward([x[b].reshape(-1) for b in range(B)], t, B, outs=o)
+        for b in range(B):
+            rel = ((o[b].reshape(4, size, size) - ref[b]).norm() / ref[b].norm()).item()
+            assert rel < 3e-2, (fold, b, rel)

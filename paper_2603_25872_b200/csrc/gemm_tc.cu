@@ -85,6 +85,7 @@ struct EpiParams {
   int out_f32;              // 1: fp32 output, 0: bf16
   int tma_store;            // 1: output written through smem staging + TMA (tmap_c)
   int hs_valid;             // DRS_ACT_HEADSOFTMAX: valid columns per 96-column head
+  int tma_res;              // 1: residual tile TMA-loaded into the staging buffer (OutMaps::r)
 };
 
 // Epilogue math on 32 consecutive accumulator columns n0..n0+31 of `row`:
@@ -101,9 +102,13 @@ __device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, f
   return true;
 }
 
+// kEpi: 0 = every activation; 1 = lean (DRS_ACT_NONE / SILU only) -- the common
+// case gets an epilogue without the GEGLU / GELU code (smaller hot loop)
+template <int kEpi>
 __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32],
-                                          const float4 (&bpre)[8], bool have_bpre) {
+                                          const float4 (&bpre)[8], bool have_bpre, bool skip_res = false) {
   const bool row_ok = row < M;
+  const void* res = skip_res ? nullptr : p.res;   // skip: added later from the TMA-loaded tile
   const bool full = n0 + 32 <= N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
@@ -129,14 +134,14 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(rb + j);
   }
-  if (p.act == DRS_ACT_GEGLU) {                // interleaved (value, gate) pairs -> N/2 outputs
+  if (kEpi == 0 && p.act == DRS_ACT_GEGLU) {   // interleaved (value, gate) pairs -> N/2 outputs
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
     const int c0 = n0 / 2;
     const bool gfull = c0 + 16 <= N / 2;
-    if (p.res && row_ok) {
+    if (res && row_ok) {
       if (p.res_f32) {
-        const float* r = static_cast<const float*>(p.res) + (int64_t)row * p.ldr + c0;
+        const float* r = static_cast<const float*>(res) + (int64_t)row * p.ldr + c0;
         if (gfull && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -148,7 +153,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
           for (int j = 0; j < 16; ++j) if (c0 + j < N / 2) v[j] += r[j];
         }
       } else {
-        const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.res) + (int64_t)row * p.ldr + c0;
+        const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(res) + (int64_t)row * p.ldr + c0;
         if (gfull && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
@@ -169,13 +174,13 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
     }
     return 16;
   }
-  if (p.act == DRS_ACT_GELU_TANH) {
+  if (kEpi == 0 && p.act == DRS_ACT_GELU_TANH) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
   } else if (p.act == DRS_ACT_SILU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = silu(v[j]);
-  } else if (p.act == DRS_ACT_GELU_ERF) {
+  } else if (kEpi == 0 && p.act == DRS_ACT_GELU_ERF) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
   }
@@ -184,8 +189,8 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] *= __ldg(cs + j);
   }
-  if (p.res && row_ok && p.res_f32) {
-    const float* r = static_cast<const float*>(p.res) + (int64_t)row * p.ldr + n0;
+  if (res && row_ok && p.res_f32) {
+    const float* r = static_cast<const float*>(res) + (int64_t)row * p.ldr + n0;
     if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -196,8 +201,8 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
 #pragma unroll
       for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += r[j];
     }
-  } else if (p.res && row_ok) {
-    const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.res) + (int64_t)row * p.ldr + n0;
+  } else if (res && row_ok) {
+    const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(res) + (int64_t)row * p.ldr + n0;
     if (full && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -254,9 +259,10 @@ __device__ __forceinline__ void epi_store_direct(const EpiParams& p, int M, int 
   }
 }
 
+template <int kEpi>
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
   float4 nob[8];
-  const int nout = epi_math32(p, M, N, row, n0, v, nob, false);
+  const int nout = epi_math32<kEpi>(p, M, N, row, n0, v, nob, false);
   const bool geglu = nout == 16;
   epi_store_direct(p, M, geglu ? N / 2 : N, row, geglu ? n0 / 2 : n0, nout, v);
 }
@@ -283,6 +289,31 @@ __device__ __forceinline__ void stage_rows(uint8_t* buf, int lane, int pitch, bo
       }
       const int off = lane * pitch + q * 16;
       *reinterpret_cast<uint4*>(buf + (off ^ (((off >> 7) & mask) << 4))) = u;
+    }
+  }
+}
+
+// v += this lane's row of a staged (TMA-loaded, same swizzle as stage_rows) tile
+__device__ __forceinline__ void add_staged_rows(const uint8_t* buf, int lane, int pitch, bool f32, float (&v)[32]) {
+  const int mask = pitch == 128 ? 7 : (pitch == 64 ? 3 : 1);
+  const int nchunk = pitch / 16;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q < nchunk) {
+      const int off = lane * pitch + q * 16;
+      const uint4 u = *reinterpret_cast<const uint4*>(buf + (off ^ (((off >> 7) & mask) << 4)));
+      if (f32) {
+        v[4 * q] += __uint_as_float(u.x); v[4 * q + 1] += __uint_as_float(u.y);
+        v[4 * q + 2] += __uint_as_float(u.z); v[4 * q + 3] += __uint_as_float(u.w);
+      } else {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
     }
   }
 }
@@ -382,7 +413,16 @@ __device__ __forceinline__ void head_softmax_row(const EpiParams& ep, int M, int
     }
 }
 
-constexpr int kStgBytes = 4096;        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
+constexpr int kStgBytes = 4096;
+
+// Output-side tensor maps: the staged TMA store (c) and, when the epilogue has
+// a residual of the output's dtype, the residual tile loaded by TMA into the
+// same staging buffer (r): one coalesced bulk load per 32 x 32 block instead
+// of 32 row-strided per-thread loads, issued before the accumulator is read.
+struct OutMaps {
+  CUtensorMap c;
+  CUtensorMap r;
+};        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
 
 template <int BN, int kStages>
 struct GemmSmem {
@@ -391,14 +431,14 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
-  static constexpr int kBytes = kBarOffset + (2 * kStages + 4) * 8 + 16 + 1024;   // +1024 alignment slack
+  static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;   // barriers; +1024 alignment slack
   static_assert(kBytes <= 227 * 1024, "GEMM shared memory plan exceeds 227 KB");
 };
 
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K, int split, EpiParams ep,
+                    const __grid_constant__ OutMaps om, int M, int N, int K, int split, EpiParams ep,
                     ConvGeom cv) {
   using S = GemmSmem<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
@@ -408,6 +448,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   uint64_t* tfull_bar = empty_bar + kStages;       // [2]
   uint64_t* tempty_bar = tfull_bar + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* res_bar = tempty_bar + 4;              // [kEpiWarps] residual tile loads
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (M + kBM - 1) / kBM, n_tiles = (N + BN - 1) / BN;
@@ -420,9 +461,11 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmap_a);
     tc::tma_prefetch(&tmap_b);
-    if (ep.tma_store) tc::tma_prefetch(&tmap_c);
+    if (ep.tma_store) tc::tma_prefetch(&om.c);
+    if (ep.tma_res) tc::tma_prefetch(&om.r);
     for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
     for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], kEpiWarps); }
+    for (int w = 0; w < kEpiWarps; ++w) tc::mbar_init(&res_bar[w], 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_slot);
@@ -507,6 +550,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     const bool dbl = pitch * 32 <= kStgBytes / 2;                 // two staging buffers fit
     uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
     int buf = 0;
+    uint32_t rph = 0;                              // res_bar phase of this warp
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int sp = tile % split;
@@ -518,7 +562,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       tc::mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const int row = mt * kBM + quad * 32 + lane;
-      if constexpr (BN == 192) {
+      if constexpr (BN == 192 && kEpi == 0) {
         if (ep.act == DRS_ACT_HEADSOFTMAX) {       // warp half h: head 2 nt + h = columns [96 h, 96 h + 96)
           head_softmax_row(ep, M, N, row, nt * BN + half * 96,
                            tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 96);
@@ -533,6 +577,12 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
         const int n0 = nt * BN + c * 32;
         float4 bpre[8];
         const bool have_b = split == 1 && n0 < N && load_bias32(ep, N, n0, bpre);
+        uint8_t* sb = stg + buf * (kStgBytes / 2);
+        if (ep.tma_res && n0 < N && lane == 0) {    // residual tile -> staging buffer, under the TMEM load
+          if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          tc::mbar_arrive_expect_tx(&res_bar[warp - 2], (uint32_t)(pitch * 32));
+          tc::tma_load_2d(&om.r, &res_bar[warp - 2], sb, n0, mt * kBM + quad * 32);
+        }
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         tc::tmem_ld_wait();
@@ -547,23 +597,28 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else if (ep.tma_store) {
-          epi_math32(ep, M, N, row, n0, v, bpre, have_b);
-          // the buffer about to be written must have been read by its last store
-          if (lane == 0) {
-            if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
+          if (ep.tma_res) {
+            tc::mbar_wait(&res_bar[warp - 2], rph);
+            rph ^= 1;
+            add_staged_rows(sb, lane, pitch, ep.out_f32 != 0, v);
+          } else {
+            // the buffer about to be written must have been read by its last store
+            if (lane == 0) {
+              if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+            }
           }
           __syncwarp();
-          uint8_t* sb = stg + buf * (kStgBytes / 2);
           stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
           fence_async_smem_g();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_c, sb, geglu ? n0 / 2 : n0, mt * kBM + quad * 32);
+            tma_store_2d(&om.c, sb, geglu ? n0 / 2 : n0, mt * kBM + quad * 32);
             bulk_commit();
           }
           if (dbl) buf ^= 1;
         } else {
-          epilogue32(ep, M, N, row, n0, v);
+          epilogue32<kEpi>(ep, M, N, row, n0, v);
         }
       }
       tc::tc_fence_before();
@@ -603,7 +658,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
             v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
           }
         }
-        epilogue32(ep, M, N, mt * kBM + r, n0, v);
+        epilogue32<kEpi>(ep, M, N, mt * kBM + r, n0, v);
       }
     }
     __syncwarp();
@@ -631,7 +686,7 @@ struct PairSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
-  static constexpr int kBytes = kBarOffset + (2 * kStages + 4) * 8 + 16 + 1024;
+  static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;
   static_assert(kBytes <= 227 * 1024, "GEMM pair shared memory plan exceeds 227 KB");
 };
 
@@ -676,10 +731,10 @@ __device__ __forceinline__ void pair_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                 const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K, EpiParams ep, ConvGeom cv) {
+                 const __grid_constant__ OutMaps om, int M, int N, int K, EpiParams ep, ConvGeom cv) {
   using S = PairSmem<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -688,6 +743,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
   uint64_t* tfull_bar = empty_bar + kStages;       // [2]
   uint64_t* tempty_bar = tfull_bar + 2;            // [2] (leader's counts both CTAs' epilogues)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* res_bar = tempty_bar + 4;              // [kEpiWarps] residual tile loads
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)pair_rank();
@@ -701,9 +757,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmap_a);
     tc::tma_prefetch(&tmap_b);
-    if (ep.tma_store) tc::tma_prefetch(&tmap_c);
+    if (ep.tma_store) tc::tma_prefetch(&om.c);
+    if (ep.tma_res) tc::tma_prefetch(&om.r);
     for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full_bar[s], 1); tc::mbar_init(&empty_bar[s], 1); }
     for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull_bar[a], 1); tc::mbar_init(&tempty_bar[a], 2 * kEpiWarps); }
+    for (int w = 0; w < kEpiWarps; ++w) tc::mbar_init(&res_bar[w], 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) {                                  // both CTAs, same warp and slot (cta_group::2 allocation)
@@ -785,6 +843,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
     const bool dbl = pitch * 32 <= kStgBytes / 2;
     uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
     int buf = 0;
+    uint32_t rph = 0;                              // res_bar phase of this warp
     int it = 0;
     for (int tile = t0; tile < num_tiles; tile += tstep, ++it) {
       const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
@@ -798,6 +857,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
         const int n0 = nt * BN + c * 32;
         float4 bpre[8];
         const bool have_b = n0 < N && load_bias32(ep, N, n0, bpre);
+        uint8_t* sb = stg + buf * (kStgBytes / 2);
+        if (ep.tma_res && n0 < N && lane == 0) {    // residual tile -> staging buffer, under the TMEM load
+          if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          tc::mbar_arrive_expect_tx(&res_bar[warp - 2], (uint32_t)(pitch * 32));
+          tc::tma_load_2d(&om.r, &res_bar[warp - 2], sb, n0, mrow0 + quad * 32);
+        }
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c * 32, r);
         tc::tmem_ld_wait();
@@ -806,22 +871,28 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if (ep.tma_store) {
-          epi_math32(ep, M, N, row, n0, v, bpre, have_b);
-          if (lane == 0) {
-            if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
+          if (ep.tma_res) {
+            tc::mbar_wait(&res_bar[warp - 2], rph);
+            rph ^= 1;
+            add_staged_rows(sb, lane, pitch, ep.out_f32 != 0, v);
+          } else {
+            // the buffer about to be written must have been read by its last store
+            if (lane == 0) {
+              if (dbl) bulk_wait_read<1>(); else bulk_wait_read<0>();
+            }
           }
           __syncwarp();
-          uint8_t* sb = stg + buf * (kStgBytes / 2);
           stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
           fence_async_smem_g();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_c, sb, geglu ? n0 / 2 : n0, mrow0 + quad * 32);
+            tma_store_2d(&om.c, sb, geglu ? n0 / 2 : n0, mrow0 + quad * 32);
             bulk_commit();
           }
           if (dbl) buf ^= 1;
         } else {
-          epilogue32(ep, M, N, row, n0, v);
+          epilogue32<kEpi>(ep, M, N, row, n0, v);
         }
       }
       tc::tc_fence_before();
@@ -854,7 +925,7 @@ __device__ __forceinline__ void mma_commit_pair_mask(uint64_t* bar, uint16_t mas
                :: "r"(tc::smem_u32(bar)), "h"(mask) : "memory");
 }
 
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        int M, int N, int K, int split, EpiParams ep, ConvGeom cv) {
@@ -994,7 +1065,7 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
         }
       }
-      epilogue32(ep, M, N, m0 + r, n0, v);
+      epilogue32<kEpi>(ep, M, N, m0 + r, n0, v);
     }
   }
   __syncwarp();
@@ -1077,12 +1148,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi>
 static bool ensure_smem_attr() {
   static int state = 0;        // 0 unknown, 1 ok, -1 failed
   if (!state) {
     using S = GemmSmem<BN, kStages>;
-    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::kBytes) == cudaSuccess ? 1 : -1;
   }
   return state > 0;
@@ -1090,14 +1161,14 @@ static bool ensure_smem_attr() {
 
 // Clusters of `split` CTAs of this configuration that fit on the GPU at once
 // (GPC packing makes this less than #SMs / split); cached per split.
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi = 1>
 static int max_clusters(int split) {
   static int cache[9] = {0};
   if (split < 2 || split > 8) return num_sms();
   if (!cache[split]) {
     using S = GemmSmem<BN, kStages>;
     int n = 0;
-    if (ensure_smem_attr<BN, kStages>()) {
+    if (ensure_smem_attr<BN, kStages, kEpi>()) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(split * 64);
       cfg.blockDim = dim3(kGemmThreads);
@@ -1109,7 +1180,7 @@ static int max_clusters(int split) {
       la[0].val.clusterDim.z = 1;
       cfg.attrs = la;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages>, &cfg) != cudaSuccess) n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages, kEpi>, &cfg) != cudaSuccess) n = 0;
       cudaGetLastError();
     }
     cache[split] = n > 0 ? n : num_sms() / split;
@@ -1117,12 +1188,12 @@ static int max_clusters(int split) {
   return cache[split];
 }
 
-template <int BN, int kStages>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, int M, int N, int K,
+template <int BN, int kStages, int kEpi>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K,
                        int split, const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
-  auto kern = gemm_bf16_tc_kernel<BN, kStages>;
-  if (!ensure_smem_attr<BN, kStages>()) return DRS_ERR_CUDA;
+  auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi>;
+  if (!ensure_smem_attr<BN, kStages, kEpi>()) return DRS_ERR_CUDA;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "split-K partial tile must fit the stage ring");
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
   if (split == 1) {
@@ -1149,11 +1220,11 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
-template <int BN, int kStages>
-static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, int M, int N, int K,
+template <int BN, int kStages, int kEpi>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K,
                        const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = PairSmem<BN, kStages>;
-  auto kern = gemm_pair_kernel<BN, kStages>;
+  auto kern = gemm_pair_kernel<BN, kStages, kEpi>;
   static int cap = 0;
   if (!cap) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
@@ -1194,12 +1265,12 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUten
 }
 
 
-template <int BN, int kStages>
+template <int BN, int kStages, int kEpi>
 static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
                              const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = PairSmem<BN, kStages>;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "pair split-K partial tile must fit the ring");
-  auto kern = gemm_pair_split_kernel<BN, kStages>;
+  auto kern = gemm_pair_split_kernel<BN, kStages, kEpi>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess ||
@@ -1224,6 +1295,32 @@ static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, split, ep, cv);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+
+template <int kEpi>
+static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
+                         int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
+  if (pair && split > 1) {
+    ep.tma_store = 0;                              // reduced rows are stored directly
+    if (bn == 64) return launch_pair_split<64, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 128) return launch_pair_split<128, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 160) return launch_pair_split<160, 7, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 192) return launch_pair_split<192, 6, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+    return launch_pair_split<256, 6, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+  }
+  if (pair) {
+    if (bn == 64) return launch_pair<64, 8, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 128) return launch_pair<128, 8, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 160) return launch_pair<160, 7, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 192) return launch_pair<192, 6, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+    return launch_pair<256, 6, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+  }
+  if (bn == 64) return launch_gemm<64, 8, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 128) return launch_gemm<128, 6, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 160) return launch_gemm<160, 5, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 192) return launch_gemm<192, 4, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  return launch_gemm<256, 4, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
 }
 
 static int max_clusters_bn(int bn, int split) {
@@ -1342,40 +1439,27 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
     return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
-  CUtensorMap tcm;
+  OutMaps tcm;
   memset(&tcm, 0, sizeof(tcm));
   {
     const int elem = g->out_f32 ? 4 : 2;
     const int n_out = g->act == DRS_ACT_GEGLU ? N / 2 : N;
     const bool ok = split == 1 && !hsm && !(reinterpret_cast<uintptr_t>(g->C) & 15) && ((g->ldc * elem) % 16) == 0 &&
                     g->ldc >= n_out;
-    if (ok && make_tmap_out(&tcm, g->C, M, n_out, g->ldc, elem, g->act == DRS_ACT_GEGLU ? 16 : 32)) ep.tma_store = 1;
+    if (ok && make_tmap_out(&tcm.c, g->C, M, n_out, g->ldc, elem, g->act == DRS_ACT_GEGLU ? 16 : 32)) ep.tma_store = 1;
+    // residual of the output's dtype: TMA-loaded into the staging buffer (DRS_TMA_RES=0 disables)
+    static const int tma_res_on = [] { const char* e = getenv("DRS_TMA_RES"); return e ? atoi(e) : 1; }();
+    if (tma_res_on && ep.tma_store && g->residual && g->act != DRS_ACT_GEGLU && (g->res_f32 != 0) == (g->out_f32 != 0) &&
+        !(reinterpret_cast<uintptr_t>(g->residual) & 15) && ((g->ldr * elem) % 16) == 0 &&
+        make_tmap_out(&tcm.r, const_cast<void*>(g->residual), M, n_out, g->ldr, elem, 32))
+      ep.tma_res = 1;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  int rc;
-  if (pair && split > 1) {
-    ep.tma_store = 0;                              // reduced rows are stored directly
-    if (bn == 64) return launch_pair_split<64, 8>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 128) return launch_pair_split<128, 8>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 160) return launch_pair_split<160, 7>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 192) return launch_pair_split<192, 6>(ta, tb, M, N, K, split, ep, cv, st);
-    return launch_pair_split<256, 6>(ta, tb, M, N, K, split, ep, cv, st);
-  }
-  if (pair) {
-    if (bn == 64) return launch_pair<64, 8>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 128) return launch_pair<128, 8>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 160) return launch_pair<160, 7>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 192) return launch_pair<192, 6>(ta, tb, tcm, M, N, K, ep, cv, st);
-    return launch_pair<256, 6>(ta, tb, tcm, M, N, K, ep, cv, st);
-  }
-  if (bn == 64) rc = launch_gemm<64, 8>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  else if (bn == 160) rc = launch_gemm<160, 5>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  else if (bn == 192) rc = launch_gemm<192, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  else rc = launch_gemm<256, 4>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  return rc;
+  if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)
+    return gemm_dispatch<1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
+  return gemm_dispatch<0>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
 }
 
 extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,

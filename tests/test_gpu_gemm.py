@@ -203,3 +203,27 @@ def test_gemm_head_softmax(cuda, M, heads, K, valid):
     err = (y.float().view(M, heads, 96) - p).abs().max().item()
     assert err <= 4e-3, err
     assert torch.all(y.view(M, heads, 96)[:, :, valid:] == 0)
+
+
+@pytest.mark.parametrize("M,N,K,bn,pair", [(256, 64, 64, 64, False), (8192, 320, 320, 160, False), (300, 200, 136, 128, False),
+                                           (2048, 640, 640, 128, True), (512, 1280, 1280, 64, True), (77, 768, 320, 192, False)])
+@pytest.mark.parametrize("f32", [False, True])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_gemm_tma_residual(cuda, M, N, K, bn, pair, f32, inplace):
+    """Residual of the output's dtype is TMA-loaded into the epilogue's staging
+    tile (also in place, out == residual as the fp32 transformer stream uses
+    it); result equals the per-thread residual path bit for bit."""
+    import os
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M * 3 + N + K)
+    dt = torch.float32 if f32 else torch.bfloat16
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    r0 = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    r = r0.clone()
+    y = linear(x, w, bias=b, residual=r, out=r if inplace else torch.empty_like(r), bn=bn, split=1, pair=pair)
+    ref = _ref(x, w, b, None, r0, 1.0)
+    tol = 1e-3 if f32 else 2e-2
+    err = (y.float() - ref).abs().max().item()
+    assert err <= tol * max(1.0, ref.abs().max().item()), err

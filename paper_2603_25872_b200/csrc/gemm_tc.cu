@@ -435,11 +435,14 @@ struct GemmSmem {
   static_assert(kBytes <= 227 * 1024, "GEMM shared memory plan exceeds 227 KB");
 };
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, bool kSplit>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ OutMaps om, int M, int N, int K, int split, EpiParams ep,
+                    const __grid_constant__ OutMaps om, int M, int N, int K, int split_arg, EpiParams ep,
                     ConvGeom cv) {
+  // kSplit: cluster split-K instantiation (one (tile, split) unit per CTA, DSMEM
+  // reduction); otherwise persistent with split == 1 known at compile time
+  const int split = kSplit ? split_arg : 1;
   using S = GemmSmem<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -589,8 +592,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
         if (n0 >= N) continue;
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = kb1 > kb0 ? __uint_as_float(r[j]) : 0.f;
-        if (split > 1) {
+        for (int j = 0; j < 32; ++j) v[j] = (!kSplit || kb1 > kb0) ? __uint_as_float(r[j]) : 0.f;
+        if (kSplit) {
           // partial tile -> this CTA's smem (padded rows: conflict-free float4 stores)
           float* dst = reinterpret_cast<float*>(smem) + (quad * 32 + lane) * (BN + 4) + c * 32;
 #pragma unroll
@@ -627,7 +630,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     }
     if (ep.tma_store && lane == 0) bulk_wait_read<0>();   // smem reads done; the writes complete with the grid
   }
-  if (split > 1) {
+  if (kSplit) {
     // ---------------- cluster split-K reduction over DSMEM ----------------
     // (non-persistent: this CTA computed exactly one (tile, split) unit; its
     // cluster rank is its split index)
@@ -1148,12 +1151,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, bool kSplit>
 static bool ensure_smem_attr() {
   static int state = 0;        // 0 unknown, 1 ok, -1 failed
   if (!state) {
     using S = GemmSmem<BN, kStages>;
-    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages, kEpi, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::kBytes) == cudaSuccess ? 1 : -1;
   }
   return state > 0;
@@ -1168,7 +1171,7 @@ static int max_clusters(int split) {
   if (!cache[split]) {
     using S = GemmSmem<BN, kStages>;
     int n = 0;
-    if (ensure_smem_attr<BN, kStages, kEpi>()) {
+    if (ensure_smem_attr<BN, kStages, kEpi, true>()) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(split * 64);
       cfg.blockDim = dim3(kGemmThreads);
@@ -1180,7 +1183,7 @@ static int max_clusters(int split) {
       la[0].val.clusterDim.z = 1;
       cfg.attrs = la;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages, kEpi>, &cfg) != cudaSuccess) n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages, kEpi, true>, &cfg) != cudaSuccess) n = 0;
       cudaGetLastError();
     }
     cache[split] = n > 0 ? n : num_sms() / split;
@@ -1192,16 +1195,18 @@ template <int BN, int kStages, int kEpi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K,
                        int split, const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
-  auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi>;
-  if (!ensure_smem_attr<BN, kStages, kEpi>()) return DRS_ERR_CUDA;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "split-K partial tile must fit the stage ring");
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
   if (split == 1) {
+    auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, false>;
+    if (!ensure_smem_attr<BN, kStages, kEpi, false>()) return DRS_ERR_CUDA;
     const int grid = tiles < num_sms() ? tiles : num_sms();
     launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
     return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
   }
   // split-K: one CTA per (tile, split), the split CTAs of a tile as one cluster
+  auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, true>;
+  if (!ensure_smem_attr<BN, kStages, kEpi, true>()) return DRS_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(kGemmThreads);

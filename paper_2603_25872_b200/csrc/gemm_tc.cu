@@ -599,7 +599,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else if (ep.tma_store) {
+        } else {                                   // persistent kernel: always the staged TMA store
           epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
           if (ep.tma_res) {
             tc::mbar_wait(&res_bar[warp - 2], rph);
@@ -620,8 +620,6 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
             bulk_commit();
           }
           if (dbl) buf ^= 1;
-        } else {
-          epilogue32<kEpi>(ep, M, N, row, n0, v);
         }
       }
       tc::tc_fence_before();
@@ -873,7 +871,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (ep.tma_store) {
+        {                                          // the host pairs only TMA-store epilogues
           epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
           if (ep.tma_res) {
             tc::mbar_wait(&res_bar[warp - 2], rph);
@@ -894,8 +892,6 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
             bulk_commit();
           }
           if (dbl) buf ^= 1;
-        } else {
-          epilogue32<kEpi>(ep, M, N, row, n0, v);
         }
       }
       tc::tc_fence_before();
@@ -1197,14 +1193,15 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMa
   using S = GemmSmem<BN, kStages>;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "split-K partial tile must fit the stage ring");
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
-  if (split == 1) {
+  if (split == 1 && (ep.tma_store || ep.act == DRS_ACT_HEADSOFTMAX)) {   // persistent: staged TMA stores
     auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, false>;
     if (!ensure_smem_attr<BN, kStages, kEpi, false>()) return DRS_ERR_CUDA;
     const int grid = tiles < num_sms() ? tiles : num_sms();
     launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
     return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
   }
-  // split-K: one CTA per (tile, split), the split CTAs of a tile as one cluster
+  // split-K (or an output the TMA store cannot address: split == 1, direct
+  // stores): one CTA per (tile, split), the split CTAs of a tile as one cluster
   auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, true>;
   if (!ensure_smem_attr<BN, kStages, kEpi, true>()) return DRS_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
@@ -1306,6 +1303,7 @@ static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M
 template <int kEpi>
 static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
                          int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
+  if (pair && split == 1 && !ep.tma_store) pair = false;      // the pair kernel stores through TMA only
   if (pair && split > 1) {
     ep.tma_store = 0;                              // reduced rows are stored directly
     if (bn == 64) return launch_pair_split<64, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);

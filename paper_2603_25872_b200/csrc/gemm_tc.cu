@@ -104,11 +104,13 @@ __device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, f
 
 // kEpi: 0 = every activation; 1 = lean (DRS_ACT_NONE / SILU only) -- the common
 // case gets an epilogue without the GEGLU / GELU code (smaller hot loop)
-template <int kEpi>
+// kFast (persistent / pair kernels): a residual, if any, always arrives through
+// the TMA-loaded staging tile, so the per-thread residual loads are compiled out
+template <int kEpi, bool kFast = false>
 __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32],
                                           const float4 (&bpre)[8], bool have_bpre, bool skip_res = false) {
   const bool row_ok = row < M;
-  const void* res = skip_res ? nullptr : p.res;   // skip: added later from the TMA-loaded tile
+  const void* res = (kFast || skip_res) ? nullptr : p.res;   // skip: added later from the TMA-loaded tile
   const bool full = n0 + 32 <= N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
@@ -600,7 +602,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {                                   // persistent kernel: always the staged TMA store
-          epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
+          epi_math32<kEpi, true>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
           if (ep.tma_res) {
             tc::mbar_wait(&res_bar[warp - 2], rph);
             rph ^= 1;
@@ -872,7 +874,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         {                                          // the host pairs only TMA-store epilogues
-          epi_math32<kEpi>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
+          epi_math32<kEpi, true>(ep, M, N, row, n0, v, bpre, have_b, ep.tma_res != 0);
           if (ep.tma_res) {
             tc::mbar_wait(&res_bar[warp - 2], rph);
             rph ^= 1;
@@ -1193,7 +1195,8 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMa
   using S = GemmSmem<BN, kStages>;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "split-K partial tile must fit the stage ring");
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
-  if (split == 1 && (ep.tma_store || ep.act == DRS_ACT_HEADSOFTMAX)) {   // persistent: staged TMA stores
+  if (split == 1 && ((ep.tma_store && (!ep.res || ep.tma_res)) || ep.act == DRS_ACT_HEADSOFTMAX)) {
+    // persistent: staged TMA stores (and TMA-loaded residual tiles)
     auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, false>;
     if (!ensure_smem_attr<BN, kStages, kEpi, false>()) return DRS_ERR_CUDA;
     const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -1303,7 +1306,6 @@ static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M
 template <int kEpi>
 static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
                          int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
-  if (pair && split == 1 && !ep.tma_store) pair = false;      // the pair kernel stores through TMA only
   if (pair && split > 1) {
     ep.tma_store = 0;                              // reduced rows are stored directly
     if (bn == 64) return launch_pair_split<64, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
@@ -1433,14 +1435,10 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
     return DRS_ERR_CUDA;
   }
-  // 2-SM pair mode: M >= 256 (split > 1: pair + cluster split-K, 2 * split <= 16 CTAs)
-  const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM));
   if (g->b_img_rows > 0) {
     cv.b_img_rows = g->b_img_rows;
     cv.b_img_off = g->b_img_off;
   }
-  if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
-    return DRS_ERR_CUDA;
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
@@ -1459,6 +1457,12 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
         make_tmap_out(&tcm.r, const_cast<void*>(g->residual), M, n_out, g->ldr, elem, 32))
       ep.tma_res = 1;
   }
+  // 2-SM pair mode: M >= 256 (split > 1: pair + cluster split-K, 2 * split <= 16 CTAs); a
+  // split == 1 pair runs the persistent TMA epilogue only (decided here: the B map's box depends on it)
+  const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM)) &&
+                    (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
+  if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
+    return DRS_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)
     return gemm_dispatch<1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);

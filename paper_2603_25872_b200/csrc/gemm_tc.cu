@@ -102,8 +102,9 @@ __device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, f
   return true;
 }
 
-// kEpi: 0 = every activation; 1 = lean (DRS_ACT_NONE / SILU only) -- the common
-// case gets an epilogue without the GEGLU / GELU code (smaller hot loop)
+// kEpi: 1 = lean (DRS_ACT_NONE / SILU), 2 = GEGLU, 0 = GELU (tanh / erf) and the
+// head softmax -- each instantiation carries only its own activation code (the
+// epilogue hot loop stays small: measured 2-5 % per network eval)
 // kFast (persistent / pair kernels): a residual, if any, always arrives through
 // the TMA-loaded staging tile, so the per-thread residual loads are compiled out
 template <int kEpi, bool kFast = false>
@@ -136,7 +137,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(rb + j);
   }
-  if (kEpi == 0 && p.act == DRS_ACT_GEGLU) {   // interleaved (value, gate) pairs -> N/2 outputs
+  if (kEpi == 2 && p.act == DRS_ACT_GEGLU) {   // interleaved (value, gate) pairs -> N/2 outputs
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
     const int c0 = n0 / 2;
@@ -179,7 +180,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
   if (kEpi == 0 && p.act == DRS_ACT_GELU_TANH) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
-  } else if (p.act == DRS_ACT_SILU) {
+  } else if (kEpi == 1 && p.act == DRS_ACT_SILU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = silu(v[j]);
   } else if (kEpi == 0 && p.act == DRS_ACT_GELU_ERF) {
@@ -550,7 +551,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     // ---------------- epilogue (warps 2..9) ----------------
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
     const int half = (warp - 2) >> 2;              // which 32-column chunks (even / odd) it drains
-    const bool geglu = ep.act == DRS_ACT_GEGLU;
+    const bool geglu = kEpi == 2 && ep.act == DRS_ACT_GEGLU;
     const int pitch = (geglu ? 16 : 32) * (ep.out_f32 ? 4 : 2);   // staged row bytes
     const bool dbl = pitch * 32 <= kStgBytes / 2;                 // two staging buffers fit
     uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
@@ -841,7 +842,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
     // ---------------- epilogue (warps 2..9 of both CTAs: own 128 rows) ----------------
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    const bool geglu = ep.act == DRS_ACT_GEGLU;
+    const bool geglu = kEpi == 2 && ep.act == DRS_ACT_GEGLU;
     const int pitch = (geglu ? 16 : 32) * (ep.out_f32 ? 4 : 2);
     const bool dbl = pitch * 32 <= kStgBytes / 2;
     uint8_t* stg = smem + S::kStgOffset + (warp - 2) * kStgBytes;
@@ -1466,6 +1467,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)
     return gemm_dispatch<1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
+  if (g->act == DRS_ACT_GEGLU) return gemm_dispatch<2>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
   return gemm_dispatch<0>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
 }
 

@@ -102,8 +102,9 @@ __device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, f
   return true;
 }
 
-// kEpi: 1 = lean (DRS_ACT_NONE / SILU), 2 = GEGLU, 0 = GELU (tanh / erf) and the
-// head softmax -- each instantiation carries only its own activation code (the
+// kEpi: 1 = lean (no activation, no per-row bias / column scale), 3 = lean +
+// SiLU + per-row-group bias / column gate, 2 = GEGLU, 0 = GELU (tanh / erf) and
+// the head softmax -- each instantiation carries only its own activation code (the
 // epilogue hot loop stays small: measured 2-5 % per network eval)
 // kFast (persistent / pair kernels): a residual, if any, always arrives through
 // the TMA-loaded staging tile, so the per-thread residual loads are compiled out
@@ -132,7 +133,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
       for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(p.bias + n0 + j);
     }
   }
-  if (p.rowbias && row_ok) {
+  if (kEpi != 1 && p.rowbias && row_ok) {
     const float* rb = p.rowbias + (int64_t)(row / p.rb_group) * p.rb_ld + n0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(rb + j);
@@ -180,14 +181,14 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
   if (kEpi == 0 && p.act == DRS_ACT_GELU_TANH) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
-  } else if (kEpi == 1 && p.act == DRS_ACT_SILU) {
+  } else if (kEpi == 3 && p.act == DRS_ACT_SILU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = silu(v[j]);
   } else if (kEpi == 0 && p.act == DRS_ACT_GELU_ERF) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
   }
-  if (p.colscale && row_ok) {
+  if (kEpi != 1 && p.colscale && row_ok) {
     const float* cs = p.colscale + (p.cs_group > 0 ? (int64_t)(row / p.cs_group) * p.cs_ld : 0) + n0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] *= __ldg(cs + j);
@@ -1465,8 +1466,10 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
     return DRS_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)
+  if (g->act == DRS_ACT_NONE && !g->rowbias && !g->colscale)
     return gemm_dispatch<1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
+  if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)
+    return gemm_dispatch<3>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
   if (g->act == DRS_ACT_GEGLU) return gemm_dispatch<2>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
   return gemm_dispatch<0>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
 }

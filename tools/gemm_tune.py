@@ -131,6 +131,8 @@ def main():
         name, bs = spec.split(":")
         for d in collect(name, [int(b) for b in bs.split(",")], dev):
             key = netops.table_key(d[0], d[1], d[2], d[7] is not None)
+            if d[3] == "headsoftmax":          # fixed tile (bn 192, 1-SM): nothing to tune
+                continue
             if not a.mmax or d[0] <= a.mmax:
                 uniq.setdefault(key, d)
     print(f"{len(uniq)} unique GEMM shapes", flush=True)

@@ -393,9 +393,11 @@ def main():
     prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(prof):
         tr = json.load(open(prof))
-        roofline["traffic"] = tr.get(roofline["kernel"])
-        if roofline["traffic"] is not None and net_cfg:
-            roofline["traffic_detail"] = tr.get("_detail")
+        # the capture is of one network's GEMMs (tools/gemm_traffic.py): only that config reports it
+        if not net_cfg or tr.get("_detail", {}).get("net", "sd15") == cfg["net"]:
+            roofline["traffic"] = tr.get(roofline["kernel"])
+            if roofline["traffic"] is not None and net_cfg:
+                roofline["traffic_detail"] = tr.get("_detail")
 
     # draft-and-refine on this one GPU (logical devices batched per round), for context
     drf = {"T": cfg["T"], "mode_timed": mode, "devices": n}

@@ -71,7 +71,7 @@ def summarise(algo_path, csv_path):
     dram = sum(r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0) for r in rows[:n])
     ab = sum(a["algo_bytes"] for a in algo[:n])
     out = {"gemm_bf16_tc_kernel (tcgen05.mma, TMA, TMEM)": dram / n,
-           "_detail": {"launches": n, "dram_bytes_per_launch": dram / n, "algorithmic_bytes_per_launch": ab / n,
+           "_detail": {"net": "sd15", "launches": n, "dram_bytes_per_launch": dram / n, "algorithmic_bytes_per_launch": ab / n,
                        "dram_over_algorithmic": dram / ab, "source": os.path.basename(csv_path),
                        "method": "ncu dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch of one SD1.5 "
                                  "forward (--cache-control none), averaged"}}

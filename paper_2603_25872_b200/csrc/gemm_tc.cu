@@ -67,6 +67,62 @@ __device__ __forceinline__ float gelu_erf(float x) {
 }
 __device__ __forceinline__ float silu(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
 
+// Two GELU(erf)s at once on the paired FP32 pipe (fma/mul.rn.f32x2 -> FFMA2 /
+// FMUL2): the same erfc rational form as gelu_erf, with log2(e) folded into the
+// polynomial so the exponential is one ex2.approx, and rcp.approx for t
+// (|error| ~1e-6 relative, far below the bf16 output rounding): ~14 instructions
+// per GELU instead of ~25 -- the GEGLU epilogue is the bound of its GEMMs.
+__device__ __forceinline__ uint64_t f2pk(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2upk(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void gelu_erf_x2(float& x0, float& x1) {
+  constexpr float L = 1.4426950408889634f;
+  const float u0 = x0 * 0.7071067811865476f, u1 = x1 * 0.7071067811865476f;
+  const float z0 = fabsf(u0), z1 = fabsf(u1);
+  const float t0 = rcp_approx(fmaf(0.5f, z0, 1.f)), t1 = rcp_approx(fmaf(0.5f, z1, 1.f));
+  const uint64_t t = f2pk(t0, t1);
+#define DRS_C2(c) f2pk((c) * L, (c) * L)
+  uint64_t p = ffma2(t, DRS_C2(0.17087277f), DRS_C2(-0.82215223f));
+  p = ffma2(t, p, DRS_C2(1.48851587f));
+  p = ffma2(t, p, DRS_C2(-1.13520398f));
+  p = ffma2(t, p, DRS_C2(0.27886807f));
+  p = ffma2(t, p, DRS_C2(-0.18628806f));
+  p = ffma2(t, p, DRS_C2(0.09678418f));
+  p = ffma2(t, p, DRS_C2(0.37409196f));
+  p = ffma2(t, p, DRS_C2(1.00002368f));
+  p = ffma2(t, p, DRS_C2(-1.26551223f));
+#undef DRS_C2
+  const uint64_t arg = ffma2(f2pk(-z0, -z1), fmul2(f2pk(z0, z1), f2pk(L, L)), p);   // log2e (-z^2 + P(t))
+  float a0, a1;
+  f2upk(arg, a0, a1);
+  const float r0 = t0 * ex2_approx(a0), r1 = t1 * ex2_approx(a1);                  // erfc(|u|)
+  const float e0 = copysignf(1.f - r0, u0), e1 = copysignf(1.f - r1, u1);
+  f2upk(fmul2(fmul2(f2pk(0.5f, 0.5f), f2pk(x0, x1)), f2pk(1.f + e0, 1.f + e1)), x0, x1);
+}
+
 struct EpiParams {
   void* out;
   int64_t ldo;
@@ -140,7 +196,12 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
   }
   if (kEpi == 2 && p.act == DRS_ACT_GEGLU) {   // interleaved (value, gate) pairs -> N/2 outputs
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = v[2 * j] * gelu_erf(v[2 * j + 1]);
+    for (int j = 0; j < 16; j += 2) {
+      float g0 = v[2 * j + 1], g1 = v[2 * j + 3];
+      gelu_erf_x2(g0, g1);
+      v[j] = v[2 * j] * g0;
+      v[j + 1] = v[2 * j + 2] * g1;
+    }
     const int c0 = n0 / 2;
     const bool gfull = c0 + 16 <= N / 2;
     if (res && row_ok) {

@@ -794,7 +794,10 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     stat[2 * g] = mean;
     stat[2 * g + 1] = rsqrtf(var + eps);
   }
-  gn_cluster_sync();
+  // peers may still read this CTA's csum: arrive now, wait only before exiting,
+  // so the apply / store below overlaps the slowest peer's DSMEM reads
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();                                       // stat[] visible CTA-wide
   if (rr < R) {
     float sa[8], sb[8];
 #pragma unroll
@@ -828,6 +831,7 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 typedef CUresult (*PFN_encodeTiledGn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -72,6 +72,10 @@ typedef struct drs_gemm_args {
   int b_img_rows, b_img_off;
   /* DRS_ACT_HEADSOFTMAX: valid columns per 96-column head block (<= 96). */
   int hs_valid;
+  /* Optional bf16 copy of an fp32 output (act none, no row bias / column gate):
+   * out2[m, n] = bf16(C[m, n]), row stride ldo2 (the transformer's residual stream
+   * and the bf16 input of the projection that follows, in one epilogue). */
+  void* out2; int64_t ldo2;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
 

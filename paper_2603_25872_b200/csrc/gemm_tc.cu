@@ -142,7 +142,29 @@ struct EpiParams {
   int tma_store;            // 1: output written through smem staging + TMA (tmap_c)
   int hs_valid;             // DRS_ACT_HEADSOFTMAX: valid columns per 96-column head
   int tma_res;              // 1: residual tile TMA-loaded into the staging buffer (OutMaps::r)
+  void* out2;               // kEpi 4: a bf16 copy of the (fp32) output, row stride ldo2
+  int64_t ldo2;
 };
+
+// kEpi 4: the finished row segment (32 values) also goes to the bf16 copy
+__device__ __forceinline__ void store_copy_bf16(const EpiParams& p, int M, int N, int row, int n0,
+                                                const float (&v)[32]) {
+  if (row >= M || n0 >= N) return;
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.out2) + (int64_t)row * p.ldo2 + n0;
+  if (n0 + 32 <= N) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(dst + 8 * q) = u;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) if (n0 + j < N) dst[j] = __float2bfloat16(v[j]);
+  }
+}
 
 // Epilogue math on 32 consecutive accumulator columns n0..n0+31 of `row`:
 // alpha, bias, row bias, activation (GEGLU folds (value, gate) pairs into 16
@@ -158,7 +180,7 @@ __device__ __forceinline__ bool load_bias32(const EpiParams& p, int N, int n0, f
   return true;
 }
 
-// kEpi: 1 = lean (no activation, no per-row bias / column scale), 3 = lean +
+// kEpi: 4 = lean + a bf16 copy of the output (EpiParams::out2); 1 = lean (no activation, no per-row bias / column scale), 3 = lean +
 // SiLU + per-row-group bias / column gate, 2 = GEGLU, 0 = GELU (tanh / erf) and
 // the head softmax -- each instantiation carries only its own activation code (the
 // epilogue hot loop stays small: measured 2-5 % per network eval)
@@ -189,7 +211,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
       for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(p.bias + n0 + j);
     }
   }
-  if (kEpi != 1 && p.rowbias && row_ok) {
+  if (kEpi != 1 && kEpi != 4 && p.rowbias && row_ok) {
     const float* rb = p.rowbias + (int64_t)(row / p.rb_group) * p.rb_ld + n0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] += __ldg(rb + j);
@@ -249,7 +271,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
   }
-  if (kEpi != 1 && p.colscale && row_ok) {
+  if (kEpi != 1 && kEpi != 4 && p.colscale && row_ok) {
     const float* cs = p.colscale + (p.cs_group > 0 ? (int64_t)(row / p.cs_group) * p.cs_ld : 0) + n0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) if (n0 + j < N) v[j] *= __ldg(cs + j);
@@ -328,6 +350,7 @@ template <int kEpi>
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int M, int N, int row, int n0, float (&v)[32]) {
   float4 nob[8];
   const int nout = epi_math32<kEpi>(p, M, N, row, n0, v, nob, false);
+  if constexpr (kEpi == 4) store_copy_bf16(p, M, N, row, n0, v);
   const bool geglu = nout == 16;
   epi_store_direct(p, M, geglu ? N / 2 : N, row, geglu ? n0 / 2 : n0, nout, v);
 }
@@ -677,6 +700,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
             }
           }
           __syncwarp();
+          if constexpr (kEpi == 4) store_copy_bf16(ep, M, N, row, n0, v);
           stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
           fence_async_smem_g();
           __syncwarp();
@@ -949,6 +973,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
             }
           }
           __syncwarp();
+          if constexpr (kEpi == 4) store_copy_bf16(ep, M, N, row, n0, v);
           stage_rows(sb, lane, pitch, ep.out_f32 != 0, v);
           fence_async_smem_g();
           __syncwarp();
@@ -1503,7 +1528,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
     cv.b_img_off = g->b_img_off;
   }
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0, g->out2, g->ldo2};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   OutMaps tcm;
   memset(&tcm, 0, sizeof(tcm));
@@ -1527,6 +1552,12 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
     return DRS_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
+  if (g->out2) {                                   // plain epilogue + bf16 copy of the fp32 output
+    if (g->act != DRS_ACT_NONE || g->rowbias || g->colscale || !g->out_f32 || (g->ldo2 % 8) ||
+        (reinterpret_cast<uintptr_t>(g->out2) & 15))
+      return DRS_ERR_VALUE;
+    return gemm_dispatch<4>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
+  }
   if (g->act == DRS_ACT_NONE && !g->rowbias && !g->colscale)
     return gemm_dispatch<1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
   if (g->act == DRS_ACT_NONE || g->act == DRS_ACT_SILU)

@@ -26,13 +26,14 @@ def _ptr(t):
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
            bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None,
-           b_img=None, hs_valid=0):
+           b_img=None, hs_valid=0, out2=None):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group.  b_img = (rows, off): rows
     of images with odd index (row // rows) use w[off + n] instead of w[n] (w holds
     N + off rows; CFG pairs with per-context weights).  act="headsoftmax": per
-    96-column head, softmax (exp2) over the first hs_valid columns."""
+    96-column head, softmax (exp2) over the first hs_valid columns.  out2: a bf16
+    tensor that also receives the (fp32) output, rounded."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
     if conv is not None:          # implicit 3x3 conv: x is NHWC (N*H*W, C), K = 9*C
         cn, ch, cw, cc = conv
@@ -77,6 +78,9 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     if b_img is not None:
         g.b_img_rows, g.b_img_off = b_img
     g.hs_valid = hs_valid
+    if out2 is not None:
+        assert out2.dtype == torch.bfloat16 and out2.stride(1) == 1 and out.dtype == torch.float32
+        g.out2, g.ldo2 = out2.data_ptr(), out2.stride(0)
     if GEMM_RECORD is not None:
         GEMM_RECORD.append((2.0 * M * N * K, _lib.DrsGemmArgs.from_buffer_copy(g)))
     if TIMERS is not None:

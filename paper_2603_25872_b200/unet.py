@@ -306,8 +306,9 @@ class UNet:
                 self._lin(att, L["o2"][0], bias=L["o2"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln3"][0], beta=L["ln3"][1], eps=1e-5)
             self._lin(n1, L["ff1"][0], bias=L["ff1"][1], act="geglu", out=ffb)
-            self._lin(ffb, L["ff2"][0], bias=L["ff2"][1], residual=s, out=s)
-        ops.cast_f32_bf16(s, sb)
+            last = L is t["layers"][-1]
+            # the last layer's FF output also writes the bf16 copy proj_out reads (no cast kernel)
+            self._lin(ffb, L["ff2"][0], bias=L["ff2"][1], residual=s, out=s, out2=sb if last else None)
         out = self.buf(out_tag or f"tx_out{c}_{HW}", (M, c))
         self._lin(sb, t["pout"][0], bias=t["pout"][1], residual=x, out=out)
         return out

@@ -227,3 +227,22 @@ def test_gemm_tma_residual(cuda, M, N, K, bn, pair, f32, inplace):
     tol = 1e-3 if f32 else 2e-2
     err = (y.float() - ref).abs().max().item()
     assert err <= tol * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M,N,K,bn,split,pair", [(8192, 320, 1280, 160, 1, False), (2048, 640, 2560, 128, 1, True),
+                                                 (512, 1280, 5120, 128, 2, True), (128, 1280, 5120, 64, 4, False),
+                                                 (300, 200, 136, 64, 1, False)])
+def test_gemm_bf16_copy_output(cuda, M, N, K, bn, split, pair):
+    """out2: the fp32 output (bias + in-place fp32 residual) and its bf16 copy
+    from one epilogue, in the persistent, pair and split-K kernels."""
+    from paper_2603_25872_b200.netops import linear
+    g = torch.Generator(device=cuda).manual_seed(M + N + K + 1)
+    x = (torch.randn(M, K, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    b = torch.randn(N, device=cuda, generator=g) * 0.1
+    s = torch.randn(M, N, device=cuda, generator=g)
+    ref = _ref(x, w, b, None, s.clone(), 1.0)
+    cp = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    linear(x, w, bias=b, residual=s, out=s, out2=cp, bn=bn, split=split, pair=pair)
+    assert (s - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+    assert torch.equal(cp, s.bfloat16())

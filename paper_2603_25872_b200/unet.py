@@ -95,6 +95,7 @@ class UNet:
         self.ctx = torch.randn(2 * cfg.ctx_len, cfg.ctx_dim, generator=I.g, device=self.device).to(torch.bfloat16)
         if cfg.add_embed_dim:
             self.add_in = torch.randn(2, cfg.add_embed_dim, generator=I.g, device=self.device).to(torch.bfloat16)
+            self.add_in_rep = self.add_in.repeat(self.max_batch, 1).contiguous()   # (uncond, cond) per image
         self.blocks = []          # ordered description of the network (built once)
         self.temb_slices = []     # (offset, c) of every resblock's time projection
         self._temb_w, self._temb_b = [], []
@@ -254,7 +255,7 @@ class UNet:
         ops.groupnorm(x, N, HW, cin, self.cfg.groups, r["gn1"][0], r["gn1"][1], hn, eps=1e-5, silu=True)
         h1 = self.buf(f"r1_{co}_{HW}", (N * HW, co))
         tb = temb_all[:, r["temb_off"]:r["temb_off"] + co]
-        self._conv3(hn, cin, None, 0, N, H, W, r["conv1"], out=h1, rowbias=tb, rb_group=HW)
+        self._conv3(hn, cin, None, 0, N, H, W, r["conv1"], out=h1, rowbias=tb, rb_group=HW * self._tg)
         hn2 = self.buf(f"gn{co}_{HW}", (N * HW, co))
         ops.groupnorm(h1, N, HW, co, self.cfg.groups, r["gn2"][0], r["gn2"][1], hn2, eps=1e-5, silu=True)
         if r["sc"] is not None:
@@ -327,24 +328,38 @@ class UNet:
         for b, x in enumerate(xs):
             ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b) * HW:(2 * b + 1) * HW])
             ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b + 1) * HW:(2 * b + 2) * HW])
-        tpair = self.buf("tpair", (N,), torch.float32)
-        tpair.view(B, 2).copy_(t_dev[:B, None].expand(B, 2))
-        tf = self.buf("tfreq", (N, cfg.channels[0]))
-        ops.timestep_embedding(tpair, cfg.channels[0], tf)
-        th = self.buf("th", (N, cfg.temb_dim))
-        self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
-        temb = self.buf("temb", (N, cfg.temb_dim), torch.float32)
         if cfg.add_embed_dim:
+            # SDXL: the added (pooled text + size) embedding differs between the CFG
+            # images, so the time embedding is per image (N rows)
+            tpair = self.buf("tpair", (N,), torch.float32)
+            tpair.view(B, 2).copy_(t_dev[:B, None].expand(B, 2))
+            tf = self.buf("tfreq", (N, cfg.channels[0]))
+            ops.timestep_embedding(tpair, cfg.channels[0], tf)
+            th = self.buf("th", (N, cfg.temb_dim))
+            self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
+            temb = self.buf("temb", (N, cfg.temb_dim), torch.float32)
             ah = self.buf("ah", (N, cfg.temb_dim))
-            self._lin(self.add_in.repeat(B, 1), p["a1"][0], bias=p["a1"][1], act="silu", out=ah)
+            self._lin(self.add_in_rep[:N], p["a1"][0], bias=p["a1"][1], act="silu", out=ah)
             aemb = self.buf("aemb", (N, cfg.temb_dim), torch.float32)
             self._lin(ah, p["a2"][0], bias=p["a2"][1], out=aemb)
             self._lin(th, p["t2"][0], bias=p["t2"][1], residual=aemb, out=temb)
+            temb_act = self.buf("temb_act", (N, cfg.temb_dim))
+            ops.silu_cast(temb, temb_act)
+            self._tg = 1                                  # temb rows per image
+            n_t = N
         else:
-            self._lin(th, p["t2"][0], bias=p["t2"][1], out=temb)
-        temb_act = self.buf("temb_act", (N, cfg.temb_dim))
-        ops.silu_cast(temb, temb_act)
-        temb_all = self.buf("temb_all", (N, self.temb_w.shape[0]), torch.float32)
+            # SD1.5: both CFG images share the timestep, so the embedding MLP runs once
+            # per pair (B rows), SiLU fused into the second linear's epilogue, and the
+            # resblocks index the per-pair row (row bias group = 2 HW)
+            tf = self.buf("tfreq", (B, cfg.channels[0]))
+            ops.timestep_embedding(t_dev[:B], cfg.channels[0], tf)
+            th = self.buf("th", (B, cfg.temb_dim))
+            self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
+            temb_act = self.buf("temb_act", (B, cfg.temb_dim))
+            self._lin(th, p["t2"][0], bias=p["t2"][1], act="silu", out=temb_act)
+            self._tg = 2
+            n_t = B
+        temb_all = self.buf("temb_all", (n_t, self.temb_w.shape[0]), torch.float32)
         self._lin(temb_act, self.temb_w, bias=self.temb_b, out=temb_all)
 
         h = self.buf("h_in", (N * HW, cfg.channels[0]))

@@ -27,6 +27,13 @@ __device__ __forceinline__ double load_eps(const drs_op& op, int64_t j) {
                     : __ldg(static_cast<const double*>(op.eps) + j);
 }
 
+// G = ops whose operands are prefetched together (<= kGroup), U = elements per
+// thread per pass (grid-stride spaced, so every load stays coalesced).  The
+// latency-bound BASELINE latents run U = 1; latents larger than one wave of
+// the GPU run U = 8 / G, so each thread keeps 8 (op, element) operand sets in
+// flight -- enough bytes outstanding per SM to stream at HBM rate despite the
+// 2-3 resident CTAs the fp64 registers allow.
+template <int G, int U>
 __global__ void __launch_bounds__(kChainThreads)
 skip_chain_kernel(const drs_op* __restrict__ ops, int n_ops, int64_t D) {
   pdl_wait();
@@ -39,57 +46,75 @@ skip_chain_kernel(const drs_op* __restrict__ ops, int n_ops, int64_t D) {
     for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
-  // Operands of up to kGroup ops are loaded up front (independent loads all
-  // in flight), then the ops run back to back on registers.  Legal because a
-  // chain never reads through memory what an earlier op of the same chain
-  // wrote (engine.DeviceRun._lower asserts it): intra-chain dependencies go
-  // through the CUR / ANCHOR registers.
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < D;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    double cur = 0.0, anchor = 0.0;
-    for (int g = 0; g < n_ops; g += kGroup) {
-      double xv[kGroup], ev[kGroup], zv[kGroup];
+  // Operands of up to G ops x U elements are loaded up front (independent
+  // loads all in flight), then the ops run back to back on registers.  Legal
+  // because a chain never reads through memory what an earlier op of the same
+  // chain wrote (engine.DeviceRun._lower asserts it): intra-chain dependencies
+  // go through the CUR / ANCHOR registers.
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < D; j0 += stride * U) {
+    double cur[U], anchor[U];
 #pragma unroll
-      for (int u = 0; u < kGroup; ++u) {
-        xv[u] = ev[u] = zv[u] = 0.0;
-        if (g + u < n_ops) {
-          const drs_op& op = s_ops[g + u];
-          if (op.src == DRS_SRC_X) xv[u] = op.x[j];
-          ev[u] = load_eps(op, j);
-          if (op.noisy) zv[u] = __ldg(op.z + j);
+    for (int e = 0; e < U; ++e) cur[e] = anchor[e] = 0.0;
+    for (int g = 0; g < n_ops; g += G) {
+      double xv[G][U], ev[G][U], zv[G][U];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+#pragma unroll
+        for (int e = 0; e < U; ++e) {
+          const int64_t j = j0 + e * stride;
+          xv[u][e] = ev[u][e] = zv[u][e] = 0.0;
+          if (g + u < n_ops && j < D) {
+            const drs_op& op = s_ops[g + u];
+            if (op.src == DRS_SRC_X) xv[u][e] = op.x[j];
+            ev[u][e] = load_eps(op, j);
+            if (op.noisy) zv[u][e] = __ldg(op.z + j);
+          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < kGroup; ++u) {
+      for (int u = 0; u < G; ++u) {
         if (g + u >= n_ops) break;
         const drs_op& op = s_ops[g + u];
-        const double x = op.src == DRS_SRC_X ? xv[u] : (op.src == DRS_SRC_CUR ? cur : anchor);
-        const double e = ev[u];
-        double y;
-        if (op.family == DRS_FAMILY_DDIM) {
-          // x0_hat = (x_t - sqrt(1-ab_t) eps) / sqrt(ab_t)                   transitions.py:176
-          // out = sqrt(ab_s) x0 + sqrt(1-ab_s-sigma^2) eps [+ sigma z]      transitions.py:177-179
-          const double x0 = (x - op.c[0] * e) / op.c[1];
-          y = op.c[2] * x0 + op.c[3] * e;
-          if (op.noisy) y = y + op.c[4] * zv[u];
-        } else if (op.family == DRS_FAMILY_DDPM || op.family == DRS_FAMILY_DDPM_X0) {
-          // x0 = predicted_x0 (sequential.py:54), or given (DDPM_X0)
-          // mean = (sqrt(r)(1-ab_s) x_t + sqrt(ab_s)(1-r) x0)/(1-ab_t) [+ sqrt(var) z]  transitions.py:115,134
-          const double x0 = op.family == DRS_FAMILY_DDPM ? (x - op.c[0] * e) / op.c[1] : e;
-          y = (op.c[2] * x + op.c[3] * x0) / op.c[4];
-          if (op.noisy) y = y + op.c[5] * zv[u];
-        } else if (op.family == DRS_FAMILY_PRED_X0) {
-          y = (x - op.c[0] * e) / op.c[1];                                   // sequential.py:54
-        } else {
-          y = x + op.c[0] * e;                                               // euler: transitions.py:188
+#pragma unroll
+        for (int e = 0; e < U; ++e) {
+          const int64_t j = j0 + e * stride;
+          if (j >= D) break;
+          const double x = op.src == DRS_SRC_X ? xv[u][e] : (op.src == DRS_SRC_CUR ? cur[e] : anchor[e]);
+          const double ep = ev[u][e];
+          double y;
+          if (op.family == DRS_FAMILY_DDIM) {
+            // x0_hat = (x_t - sqrt(1-ab_t) eps) / sqrt(ab_t)                   transitions.py:176
+            // out = sqrt(ab_s) x0 + sqrt(1-ab_s-sigma^2) eps [+ sigma z]      transitions.py:177-179
+            const double x0 = (x - op.c[0] * ep) / op.c[1];
+            y = op.c[2] * x0 + op.c[3] * ep;
+            if (op.noisy) y = y + op.c[4] * zv[u][e];
+          } else if (op.family == DRS_FAMILY_DDPM || op.family == DRS_FAMILY_DDPM_X0) {
+            // x0 = predicted_x0 (sequential.py:54), or given (DDPM_X0)
+            // mean = (sqrt(r)(1-ab_s) x_t + sqrt(ab_s)(1-r) x0)/(1-ab_t) [+ sqrt(var) z]  transitions.py:115,134
+            const double x0 = op.family == DRS_FAMILY_DDPM ? (x - op.c[0] * ep) / op.c[1] : ep;
+            y = (op.c[2] * x + op.c[3] * x0) / op.c[4];
+            if (op.noisy) y = y + op.c[5] * zv[u][e];
+          } else if (op.family == DRS_FAMILY_PRED_X0) {
+            y = (x - op.c[0] * ep) / op.c[1];                                  // sequential.py:54
+          } else {
+            y = x + op.c[0] * ep;                                              // euler: transitions.py:188
+          }
+          cur[e] = y;
+          if (op.flags & DRS_OP_SAVE_ANCHOR) anchor[e] = y;
+          if (op.out) op.out[j] = y;
+          if (op.out2) op.out2[j] = y;
         }
-        cur = y;
-        if (op.flags & DRS_OP_SAVE_ANCHOR) anchor = y;
-        if (op.out) op.out[j] = y;
-        if (op.out2) op.out2[j] = y;
       }
     }
   }
+}
+
+template <int G, int U>
+static void launch_chain_gu(const drs_op* ops, int n_ops, int64_t D, cudaStream_t st) {
+  int64_t blocks = (D + (int64_t)kChainThreads * U - 1) / ((int64_t)kChainThreads * U);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  launch_pdl(skip_chain_kernel<G, U>, dim3((unsigned)blocks), dim3(kChainThreads), 0, st, ops, n_ops, D);
 }
 
 }  // namespace drs
@@ -98,8 +123,13 @@ extern "C" int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* str
   if (n_ops < 0 || n_ops > drs::kMaxOps || D < 0) return DRS_ERR_VALUE;
   if (n_ops == 0 || D == 0) return DRS_OK;
   if (!ops) return DRS_ERR_VALUE;
-  int64_t blocks = (D + drs::kChainThreads - 1) / drs::kChainThreads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  drs::launch_pdl(drs::skip_chain_kernel, dim3((unsigned)blocks), dim3(drs::kChainThreads), 0, (cudaStream_t)stream, ops, n_ops, D);
+  cudaStream_t st = (cudaStream_t)stream;
+  // one full wave of 256-thread CTAs at 8 per SM: below it the launch is
+  // latency-bound and the widest grid (U = 1) wins
+  const bool wide = D >= (int64_t)148 * 8 * drs::kChainThreads;
+  if (n_ops >= drs::kGroup) drs::launch_chain_gu<drs::kGroup, 1>(ops, n_ops, D, st);
+  else if (n_ops >= 4) wide ? drs::launch_chain_gu<4, 2>(ops, n_ops, D, st) : drs::launch_chain_gu<4, 1>(ops, n_ops, D, st);
+  else if (n_ops >= 2) wide ? drs::launch_chain_gu<2, 4>(ops, n_ops, D, st) : drs::launch_chain_gu<2, 1>(ops, n_ops, D, st);
+  else wide ? drs::launch_chain_gu<1, 8>(ops, n_ops, D, st) : drs::launch_chain_gu<1, 1>(ops, n_ops, D, st);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

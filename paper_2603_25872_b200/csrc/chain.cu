@@ -30,9 +30,9 @@ __device__ __forceinline__ double load_eps(const drs_op& op, int64_t j) {
 // G = ops whose operands are prefetched together (<= kGroup), U = elements per
 // thread per pass (grid-stride spaced, so every load stays coalesced).  The
 // latency-bound BASELINE latents run U = 1; latents larger than one wave of
-// the GPU run U = 8 / G, so each thread keeps 8 (op, element) operand sets in
-// flight -- enough bytes outstanding per SM to stream at HBM rate despite the
-// 2-3 resident CTAs the fp64 registers allow.
+// the GPU run multi-op chains at U = 2.  G is the smallest group covering the
+// launch's ops (up to kGroup), so one-op launches do not pay the registers of
+// 8 prefetched operand sets.
 template <int G, int U>
 __global__ void __launch_bounds__(kChainThreads)
 skip_chain_kernel(const drs_op* __restrict__ ops, int n_ops, int64_t D) {
@@ -127,9 +127,13 @@ extern "C" int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* str
   // one full wave of 256-thread CTAs at 8 per SM: below it the launch is
   // latency-bound and the widest grid (U = 1) wins
   const bool wide = D >= (int64_t)148 * 8 * drs::kChainThreads;
+  // measured at D = 2^25 (tools/sampler_roofline.py, profiles/r1_sampler_roofline_v12.txt): one-op
+  // launches stream best at U = 1 (36 registers, full occupancy); chains of
+  // 2-3 ops at G = 2, U = 2; occupancy, not bytes in flight per thread, is what
+  // the fp64 operand arrays cost
   if (n_ops >= drs::kGroup) drs::launch_chain_gu<drs::kGroup, 1>(ops, n_ops, D, st);
   else if (n_ops >= 4) wide ? drs::launch_chain_gu<4, 2>(ops, n_ops, D, st) : drs::launch_chain_gu<4, 1>(ops, n_ops, D, st);
-  else if (n_ops >= 2) wide ? drs::launch_chain_gu<2, 4>(ops, n_ops, D, st) : drs::launch_chain_gu<2, 1>(ops, n_ops, D, st);
-  else wide ? drs::launch_chain_gu<1, 8>(ops, n_ops, D, st) : drs::launch_chain_gu<1, 1>(ops, n_ops, D, st);
+  else if (n_ops >= 2) wide ? drs::launch_chain_gu<2, 2>(ops, n_ops, D, st) : drs::launch_chain_gu<2, 1>(ops, n_ops, D, st);
+  else drs::launch_chain_gu<1, 1>(ops, n_ops, D, st);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

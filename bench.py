@@ -78,6 +78,39 @@ def _gemm_replay_ms(rec, dev, warm=3, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
+def _sampler_hbm(dev, peaks, log2d=25):
+    """HBM roofline of the refine kernel (K3 skip chain, one DDPM noisy op, fp32
+    eps: 8 x + 4 eps + 8 z + 8 out = 28 B/element) on a 2^25-element latent,
+    where it is bandwidth-bound (the BASELINE latents are latency-bound)."""
+    import torch
+
+    import paper_2603_25872_b200 as P
+    from paper_2603_25872_b200 import _lib
+    from paper_2603_25872_b200.transitions import ddpm_op_coeffs, launch_chain, make_op, ops_to_device
+    D = 1 << log2d
+    x = torch.randn(D, dtype=torch.float64, device=dev)
+    eps = torch.randn(D, dtype=torch.float32, device=dev)
+    z = torch.randn(D, dtype=torch.float64, device=dev)
+    out = torch.empty(D, dtype=torch.float64, device=dev)
+    c, noisy = ddpm_op_coeffs(P.default_schedule(50), 40, 2)
+    od = ops_to_device([make_op(c, _lib.FAMILY_DDPM, noisy, x=x, eps=eps, z=z, out=out)], dev)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(5):
+        launch_chain(od, 1, D, stream=st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(20):
+        launch_chain(od, 1, D, stream=st)
+    e1.record(st)
+    e1.synchronize()
+    us = e0.elapsed_time(e1) / 20 * 1e3
+    gbs = 28 * D / (us * 1e-6) / 1e9
+    del x, eps, z, out
+    return {"kernel": "skip_chain_kernel (DDPM noisy op, fp32 eps)", "elements": D, "algo_bytes_per_element": 28,
+            "avg_launch_us": us, "achieved": gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+            "frac": gbs / peaks.get("hbm_gbs"), "inputs": "2^25-element fp64 latent (> L2), 5 warm + 20 timed launches"}
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -398,6 +431,9 @@ def main():
             roofline["traffic"] = tr.get(roofline["kernel"])
             if roofline["traffic"] is not None and net_cfg:
                 roofline["traffic_detail"] = tr.get("_detail")
+
+    if world == 1 and rank == 0:
+        roofline["sampler_hbm"] = _sampler_hbm(dev, peaks)
 
     # draft-and-refine on this one GPU (logical devices batched per round), for context
     drf = {"T": cfg["T"], "mode_timed": mode, "devices": n}

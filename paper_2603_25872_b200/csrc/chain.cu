@@ -28,11 +28,9 @@ __device__ __forceinline__ double load_eps(const drs_op& op, int64_t j) {
 }
 
 // G = ops whose operands are prefetched together (<= kGroup), U = elements per
-// thread per pass (grid-stride spaced, so every load stays coalesced).  The
-// latency-bound BASELINE latents run U = 1; latents larger than one wave of
-// the GPU run multi-op chains at U = 2.  G is the smallest group covering the
-// launch's ops (up to kGroup), so one-op launches do not pay the registers of
-// 8 prefetched operand sets.
+// thread per pass (grid-stride spaced, so every load stays coalesced).  All
+// launches run U = 1 (more elements per thread lost to the occupancy their
+// registers cost); see drs_skip_chain for the choice of G.
 template <int G, int U>
 __global__ void __launch_bounds__(kChainThreads)
 skip_chain_kernel(const drs_op* __restrict__ ops, int n_ops, int64_t D) {
@@ -124,16 +122,16 @@ extern "C" int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* str
   if (n_ops == 0 || D == 0) return DRS_OK;
   if (!ops) return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
-  // one full wave of 256-thread CTAs at 8 per SM: below it the launch is
-  // latency-bound and the widest grid (U = 1) wins
+  // Latents larger than one full wave (256-thread CTAs, 8 per SM) are HBM-bound:
+  // one element and one op's operands per thread at a time (36 registers, full
+  // occupancy) streams best for every chain length measured at D = 2^25
+  // (tools/sampler_roofline.py: 1, 3, 6, 10 ops at 0.69-0.77 / 0.61 / 0.55 /
+  // 0.54 of HBM vs 0.36 / 0.36 / 0.34 with operand groups of 8).  Smaller,
+  // latency-bound latents prefetch the operands of up to kGroup ops together.
   const bool wide = D >= (int64_t)148 * 8 * drs::kChainThreads;
-  // measured at D = 2^25 (tools/sampler_roofline.py, profiles/r1_sampler_roofline_v12.txt): one-op
-  // launches stream best at U = 1 (36 registers, full occupancy); chains of
-  // 2-3 ops at G = 2, U = 2; occupancy, not bytes in flight per thread, is what
-  // the fp64 operand arrays cost
-  if (n_ops >= drs::kGroup) drs::launch_chain_gu<drs::kGroup, 1>(ops, n_ops, D, st);
-  else if (n_ops >= 4) wide ? drs::launch_chain_gu<4, 2>(ops, n_ops, D, st) : drs::launch_chain_gu<4, 1>(ops, n_ops, D, st);
-  else if (n_ops >= 2) wide ? drs::launch_chain_gu<2, 2>(ops, n_ops, D, st) : drs::launch_chain_gu<2, 1>(ops, n_ops, D, st);
-  else drs::launch_chain_gu<1, 1>(ops, n_ops, D, st);
+  if (wide || n_ops == 1) drs::launch_chain_gu<1, 1>(ops, n_ops, D, st);
+  else if (n_ops >= drs::kGroup) drs::launch_chain_gu<drs::kGroup, 1>(ops, n_ops, D, st);
+  else if (n_ops >= 4) drs::launch_chain_gu<4, 1>(ops, n_ops, D, st);
+  else drs::launch_chain_gu<2, 1>(ops, n_ops, D, st);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -82,6 +82,20 @@ def main():
         c, noisy = ddpm_op_coeffs(s, 40, 1 + i)
         ops.append(make_op(c, _lib.FAMILY_DDPM, noisy, x=x, eps=e64, z=z[i], out=outs[i]))
     chain("skip_chain 3 DDPM drafts from one anchor", ops, 64)
+    if True:                                            # longer draft fans on D/4
+        zz = torch.randn(10, D // 4, dtype=torch.float64, device=dev)
+        oo = torch.empty(10, D // 4, dtype=torch.float64, device=dev)
+        xq, eq = x[:D // 4], e64[:D // 4]
+        for k in (6, 10):
+            ops = []
+            for i in range(k):
+                c, noisy = ddpm_op_coeffs(s, 40, 1 + i)
+                ops.append(make_op(c, _lib.FAMILY_DDPM, noisy, x=xq, eps=eq, z=zz[i], out=oo[i]))
+            od = ops_to_device(ops, dev)
+            t = timeit(lambda: launch_chain(od, k, D // 4))
+            bpe = 16 + 16 * k
+            gbs = bpe * (D // 4) / t / 1e9
+            rows.append((f"skip_chain {k} DDPM drafts (D/4)", bpe, t * 1e6, gbs, gbs / peak))
 
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     for gen in ("pcg64", "sfc64"):

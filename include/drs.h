@@ -103,11 +103,12 @@ typedef struct drs_op {
 int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* stream);
 
 /* ---- toy eps oracle (K9) ------------------------------------------------- */
+#define DRS_GM_MAX_COMP 1920   /* mixture components per launch (shared-memory bound) */
 /* Gaussian-mixture eps (denoiser.py:73-107) for rows r < n_rows:
  *   x = xs[r] (fp64, D), t = ts[r] (DEVICE int32), abar = alpha_bar[t]
  *   eps[r] = -sqrt(1-abar) * sum_i resp_i(x) (sqrt(abar) m_i - x)/s_i,
  *   s_i = abar v_i + 1-abar.  means: n_comp x D fp64, logw/var: n_comp fp64.
- * xs / out are DEVICE arrays of n_rows pointers.  n_comp <= 8. */
+ * xs / out are DEVICE arrays of n_rows pointers.  1 <= n_comp <= 1920 (DRS_GM_MAX_COMP). */
 int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows, int64_t D,
                const double* alpha_bar, int T, const double* means, const double* log_w,
                const double* var, int n_comp, double* const* out, int* err, void* stream);

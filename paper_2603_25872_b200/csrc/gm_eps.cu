@@ -30,7 +30,8 @@ namespace drs {
 
 constexpr int kGmThreads = 1024;
 constexpr int kGmPer = 4;            // elements per thread held in registers
-constexpr int kGmMaxComp = 8;
+constexpr int kGmMaxComp = 8;          // components reduced per sweep over the row
+constexpr int kGmCompLimit = 1920;     // 3 x 8 B x n_comp dynamic + 2 KB static shared memory <= 48 KB
 constexpr int kGmRegComp = 2;        // components kept in registers (others re-read)
 
 template <bool VE>
@@ -42,7 +43,10 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
   pdl_wait();
   pdl_trigger();
   __shared__ double red[kGmMaxComp][32];
-  __shared__ double s_r[kGmMaxComp];
+  extern __shared__ double s_dyn[];          // n_comp log-weights, responsibilities, scales
+  double* s_lc = s_dyn;
+  double* s_r = s_dyn + n_comp;
+  double* s_sc = s_dyn + 2 * n_comp;
   const int row = blockIdx.x;
   const int t = ts[row];
   if (t < 0 || t > T) {               // TimestepOutOfRange (denoiser.py:95-96)
@@ -65,82 +69,80 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
   const int64_t chunk = (int64_t)kGmThreads * kGmPer;
   const bool single = D <= chunk;
 
-  // ---- pass 1: squared distances ------------------------------------------
-  double part[kGmMaxComp];
-#pragma unroll
-  for (int i = 0; i < kGmMaxComp; ++i) part[i] = 0.0;
+  // ---- pass 1: squared distances, kGmMaxComp components per sweep -----------
+  // (one sweep for the usual n_comp <= 8; larger mixtures re-read x per sweep)
   double xr[kGmPer], mr[kGmRegComp][kGmPer];
-  for (int64_t base = 0; base < D; base += chunk) {
+  for (int c0 = 0; c0 < n_comp; c0 += kGmMaxComp) {
+    const int nc = min(kGmMaxComp, n_comp - c0);
+    const double* __restrict__ mc = means + (int64_t)c0 * D;
+    double part[kGmMaxComp];
 #pragma unroll
-    for (int e = 0; e < kGmPer; ++e) {
-      const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
-      const bool ok = j < D;
-      xr[e] = ok ? __ldg(x + j) : 0.0;
+    for (int i = 0; i < kGmMaxComp; ++i) part[i] = 0.0;
+    for (int64_t base = 0; base < D; base += chunk) {
 #pragma unroll
-      for (int i = 0; i < kGmRegComp; ++i)
-        mr[i][e] = (ok && i < n_comp) ? __ldg(means + (int64_t)i * D + j) : 0.0;
-    }
+      for (int e = 0; e < kGmPer; ++e) {
+        const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+        const bool ok = j < D;
+        xr[e] = ok ? __ldg(x + j) : 0.0;
 #pragma unroll
-    for (int e = 0; e < kGmPer; ++e) {
-      const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
-      if (j < D) {
+        for (int i = 0; i < kGmRegComp; ++i)
+          mr[i][e] = (ok && i < nc) ? __ldg(mc + (int64_t)i * D + j) : 0.0;
+      }
 #pragma unroll
-        for (int i = 0; i < kGmMaxComp; ++i) {
-          if (i < n_comp) {
-            const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
-            const double d = xr[e] - sa * m;
-            part[i] += d * d;
+      for (int e = 0; e < kGmPer; ++e) {
+        const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
+        if (j < D) {
+#pragma unroll
+          for (int i = 0; i < kGmMaxComp; ++i) {
+            if (i < nc) {
+              const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(mc + (int64_t)i * D + j);
+              const double d = xr[e] - sa * m;
+              part[i] += d * d;
+            }
           }
         }
       }
     }
-  }
-#pragma unroll
-  for (int i = 0; i < kGmMaxComp; ++i) {
-    if (i < n_comp) {
-      double v = part[i];
-      for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) red[i][warp] = v;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    double lc[kGmMaxComp];
-    double mx = -INFINITY;
 #pragma unroll
     for (int i = 0; i < kGmMaxComp; ++i) {
-      if (i < n_comp) {
-        double d2 = red[i][lane];
-        for (int off = 16; off; off >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, off);
-        const double s = VE ? var[i] + one_m : abar * var[i] + one_m;
-        lc[i] = log_w[i] + ((-0.5 * d2) / s - (0.5 * (double)D) * log(s));
-        mx = fmax(mx, lc[i]);
-      } else {
-        lc[i] = -INFINITY;
+      if (i < nc) {
+        double v = part[i];
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) red[i][warp] = v;
       }
     }
-    if (lane == 0) {
-      double sum = 0.0;
+    __syncthreads();
+    if (warp == 0) {
 #pragma unroll
-      for (int i = 0; i < kGmMaxComp; ++i) if (i < n_comp) sum += exp(lc[i] - mx);
-      const double lse = log(sum) + mx;
-#pragma unroll
-      for (int i = 0; i < kGmMaxComp; ++i) if (i < n_comp) s_r[i] = exp(lc[i] - lse);
+      for (int i = 0; i < kGmMaxComp; ++i) {
+        if (i < nc) {
+          double d2 = red[i][lane];
+          for (int off = 16; off; off >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, off);
+          const double s = VE ? var[c0 + i] + one_m : abar * var[c0 + i] + one_m;
+          if (lane == 0) s_lc[c0 + i] = log_w[c0 + i] + ((-0.5 * d2) / s - (0.5 * (double)D) * log(s));
+        }
+      }
     }
+    __syncthreads();                       // red[] is reused by the next sweep
+  }
+  if (threadIdx.x == 0) {                  // logsumexp in component order (scipy: max, sum exp, log)
+    double mx = -INFINITY;
+    for (int i = 0; i < n_comp; ++i) mx = fmax(mx, s_lc[i]);
+    double sum = 0.0;
+    for (int i = 0; i < n_comp; ++i) sum += exp(s_lc[i] - mx);
+    const double lse = log(sum) + mx;
+    for (int i = 0; i < n_comp; ++i) s_r[i] = exp(s_lc[i] - lse);
+  }
+  for (int i = threadIdx.x; i < n_comp; i += blockDim.x) {
+    const double sc = VE ? var[i] + one_m : abar * var[i] + one_m;
+    s_sc[i] = VE ? var[i] / sc : sc;       // VE: posterior gain v_i / s_i
   }
   __syncthreads();
 
   // ---- pass 2: eps ----------------------------------------------------------
   const double neg_sq = VE ? 0.0 : -sqrt(one_m);
-  double r[kGmMaxComp], sc[kGmMaxComp];
-#pragma unroll
-  for (int i = 0; i < kGmMaxComp; ++i) {
-    r[i] = i < n_comp ? s_r[i] : 0.0;
-    sc[i] = i < n_comp ? (VE ? var[i] + one_m : abar * var[i] + one_m) : 1.0;
-    if (VE) sc[i] = i < n_comp ? var[i] / sc[i] : 0.0;   // posterior gain v_i / s_i
-  }
   for (int64_t base = 0; base < D; base += chunk) {
-    if (!single) {   // re-read this chunk (L2-resident) into the registers
+    if (!single || n_comp > kGmMaxComp) {   // re-read this chunk (L2-resident) into the registers
 #pragma unroll
       for (int e = 0; e < kGmPer; ++e) {
         const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
@@ -156,13 +158,11 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
       const int64_t j = base + (int64_t)e * kGmThreads + threadIdx.x;
       if (j < D) {
         double score = 0.0;
-#pragma unroll
-        for (int i = 0; i < kGmMaxComp; ++i) {
-          if (i < n_comp) {
-            const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
-            const double term = VE ? r[i] * (m + sc[i] * (xr[e] - m)) : (r[i] * (sa * m - xr[e])) / sc[i];
-            score = (i == 0) ? term : score + term;
-          }
+        for (int i = 0; i < n_comp; ++i) {
+          const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
+          const double r = s_r[i], sc = s_sc[i];
+          const double term = VE ? r * (m + sc * (xr[e] - m)) : (r * (sa * m - xr[e])) / sc;
+          score = (i == 0) ? term : score + term;
         }
         out[j] = VE ? (xr[e] - score) / sigma : neg_sq * score;
       }
@@ -170,15 +170,17 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
   }
 }
 
+static size_t gm_smem(int n_comp) { return (size_t)3 * sizeof(double) * n_comp; }
+
 }  // namespace drs
 
 extern "C" int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows, int64_t D,
                           const double* alpha_bar, int T, const double* means, const double* log_w,
                           const double* var, int n_comp, double* const* out, int* err, void* stream) {
-  if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmMaxComp || T < 0) return DRS_ERR_VALUE;
+  if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmCompLimit || T < 0) return DRS_ERR_VALUE;
   if (n_rows == 0 || D == 0) return DRS_OK;
   if (!xs || !ts || !alpha_bar || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
-  drs::launch_pdl(drs::gm_eps_kernel<false>, dim3(n_rows), dim3(drs::kGmThreads), 0, (cudaStream_t)stream,
+  drs::launch_pdl(drs::gm_eps_kernel<false>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
       xs, ts, D, alpha_bar, T, means, log_w, var, n_comp, out, err);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
@@ -186,10 +188,10 @@ extern "C" int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows
 extern "C" int drs_gm_velocity(const double* const* xs, const int32_t* idx, int n_rows, int64_t D,
                                const double* sigmas, int N, const double* means, const double* log_w,
                                const double* var, int n_comp, double* const* out, int* err, void* stream) {
-  if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmMaxComp || N < 0) return DRS_ERR_VALUE;
+  if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmCompLimit || N < 0) return DRS_ERR_VALUE;
   if (n_rows == 0 || D == 0) return DRS_OK;
   if (!xs || !idx || !sigmas || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
-  drs::launch_pdl(drs::gm_eps_kernel<true>, dim3(n_rows), dim3(drs::kGmThreads), 0, (cudaStream_t)stream,
+  drs::launch_pdl(drs::gm_eps_kernel<true>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
       xs, idx, D, sigmas, N, means, log_w, var, n_comp, out, err);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -27,6 +27,7 @@ from .schedule import NoiseSchedule
 
 _STATE_INDEP_SALT = 0x51DE       # denoiser.py:22
 _SEED_MASK32 = 0xFFFFFFFF        # denoiser.py:144
+GM_MAX_COMP = 1920               # include/drs.h DRS_GM_MAX_COMP
 
 
 @dataclass(frozen=True, eq=False)
@@ -48,6 +49,9 @@ class GaussianMixture:
             raise ValueError("variances must be positive")
         if len(w) != m.shape[0] or len(w) != len(v):
             raise DimensionMismatch("weights/means/variances lengths disagree")
+        if len(w) > GM_MAX_COMP:       # K9 keeps per-component scalars in shared memory
+            raise ValueError(f"{len(w)} mixture components exceed the device eps kernel's "
+                             f"limit of {GM_MAX_COMP} (include/drs.h DRS_GM_MAX_COMP)")
         object.__setattr__(self, "weights", w)
         object.__setattr__(self, "means", m)
         object.__setattr__(self, "variances", v)
@@ -178,6 +182,17 @@ class _DevKeys:
         self.dev, self.n = dev, n
 
 
+def perturb_launch_pieces(n_ops: int, n_scales: int, limit: int = 64) -> list:
+    """(offset, count) launches of a perturbation op list: row i owns ops
+    [i*S, (i+1)*S), and every op of a row after its first reads the CUR
+    register, so launches (<= limit ops, csrc/chain.cu kMaxOps) are cut at row
+    boundaries only."""
+    if n_scales > limit:
+        raise ValueError(f"{n_scales} nested Perturbed layers exceed one chain launch ({limit})")
+    per = (limit // n_scales) * n_scales
+    return [(off, min(per, n_ops - off)) for off in range(0, n_ops, per)]
+
+
 class PerturbPlan:
     """Device resources adding every Perturbed layer's pseudo-noise to eps rows:
     outs[i] += scale * default_rng(blake2b(state_i, t_i)).standard_normal(D)
@@ -199,6 +214,9 @@ class PerturbPlan:
                                    eps=self.noise[i], out=outs[i]))
         self.n_ops = len(ops)
         self.ops = ops_to_device(ops, device)
+        # a row's ops after the first read the CUR register: launches are cut at
+        # row boundaries only (<= 64 ops, csrc/chain.cu kMaxOps)
+        self.pieces = perturb_launch_pieces(self.n_ops, len(scales))
 
     def launch(self, err, stream=None):
         from .rng import fill_streams
@@ -208,9 +226,8 @@ class PerturbPlan:
                                       self.keys.data_ptr(), sp), "drs_perturb_keys")
         fill_streams(_DevKeys(self.keys, self.n), self.D, self.noise, "pcg64", err=err, stream=stream)
         size = _lib.ctypes.sizeof(_lib.DrsOp)
-        for off in range(0, self.n_ops, 64):
-            _lib.check(L.drs_skip_chain(self.ops.data_ptr() + off * size, min(64, self.n_ops - off), self.D, sp),
-                       "drs_skip_chain")
+        for off, n in self.pieces:
+            _lib.check(L.drs_skip_chain(self.ops.data_ptr() + off * size, n, self.D, sp), "drs_skip_chain")
 
 
 def apply_perturbations(scales, x, t: int, value):

@@ -38,8 +38,12 @@ def _worker_cap(requested: int) -> int:
 
 
 def _numel(x):
+    """Elements of an array-like x_T (tensor, ndarray, nested list: np.asarray semantics)."""
+    if not hasattr(x, "shape"):
+        import numpy as np
+        x = np.asarray(x, dtype=float)
     n = 1
-    for d in getattr(x, "shape", ()):
+    for d in x.shape:
         n *= int(d)
     return n
 
@@ -77,10 +81,10 @@ def execute_round(d, s, tasks: list, devices: int, *, anchor_t: int, pool=None, 
     for i, (x, t) in enumerate(tasks):
         try:
             results[i] = evaluate(core, s, x, t)
-            if scales:
+            if scales:          # the perturbation chain runs on fp64 rows (network eps is fp32)
                 results[i] = apply_perturbations(scales, torch.as_tensor(x, dtype=torch.float64,
                                                                          device=results[i].device),
-                                                 t, results[i].clone())
+                                                 t, results[i].to(torch.float64).contiguous().clone())
         except Exception as exc:      # drain the round before raising (parallel.py:168-179)
             if error is None:
                 error = exc
@@ -95,8 +99,10 @@ def execute_round(d, s, tasks: list, devices: int, *, anchor_t: int, pool=None, 
 
 
 def _check_workers(workers, submit_order_seed):
-    if workers is not None and workers < 1:
-        raise InvalidPlanParams(f"workers must be >= 1, got {workers}")
+    """`workers or devices` sizes the reference's pool (parallel.py:269): None and
+    0 both mean one worker per device; negative counts are rejected."""
+    if workers is not None and workers < 0:
+        raise InvalidPlanParams(f"workers must be >= 0, got {workers}")
 
 
 def _run(mode: Mode, s, d, x_T, devices, rule, stream, clock, workers, submit_order_seed,

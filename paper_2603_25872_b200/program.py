@@ -184,8 +184,43 @@ class _Builder:
         return r
 
     def chain(self, ops):
-        if ops:
-            self.steps.append(Chain(ops))
+        for piece in split_chain(ops):
+            self.steps.append(Chain(piece))
+
+
+CHAIN_MAX_OPS = 64        # ops per drs_skip_chain launch (csrc/chain.cu kMaxOps)
+
+
+def split_chain(ops, limit: int = CHAIN_MAX_OPS) -> list:
+    """Cut a fused op list into launches of <= limit ops.  Inside a launch the
+    CUR / ANCHOR registers carry the running state; an op that would read a
+    register set in an EARLIER launch reads the buffer that op stored instead
+    (every chained state is also written to HBM: a trajectory slot or a draft
+    row), which is the same value bit for bit.  A long aggressive refine chain
+    (k-1 refines + the next block's k2 drafts, e.g. 65 ops at T=100 with 33
+    devices) thus runs as several launches instead of failing."""
+    from dataclasses import replace
+    if len(ops) <= limit:
+        return [ops] if ops else []
+    pieces, prev_buf = [], None
+    anchor_buf, anchor_piece = None, -1
+    for p0 in range(0, len(ops), limit):
+        piece, pi = [], p0 // limit
+        for j, o in enumerate(ops[p0:p0 + limit]):
+            if o.src == _lib.SRC_CUR and j == 0:
+                if prev_buf is None:
+                    raise PlanMismatch("chain split: running state was never stored")
+                o = replace(o, src=_lib.SRC_X, x=prev_buf)
+            elif o.src == _lib.SRC_ANCHOR and anchor_piece < pi:
+                if anchor_buf is None:
+                    raise PlanMismatch("chain split: anchor state was never stored")
+                o = replace(o, src=_lib.SRC_X, x=anchor_buf)
+            piece.append(o)
+            prev_buf = o.out if o.out is not None else o.out2
+            if o.save_anchor:
+                anchor_buf, anchor_piece = prev_buf, pi
+        pieces.append(piece)
+    return pieces
 
 
 def _draft_key(t, i):

@@ -1,6 +1,7 @@
 """Single-stream samplers: the 1-GPU baseline the parallel schedulers are
 measured against (skipdiff sequential.py:57-130), as device programs."""
 
+from .parallel import _numel          # np.asarray semantics for array-like x_T
 from .program import build_sequential
 from .rng import RngStream
 from .runner import Trajectory, execute, get_run, resolve_device
@@ -12,11 +13,6 @@ def predicted_x0(s, x_t, eps, t: int):
     return predicted_x0_device(s, x_t, eps, t)
 
 
-def _numel(x):
-    n = 1
-    for d in getattr(x, "shape", ()):
-        n *= int(d)
-    return n
 
 
 def sample_ddpm(s, d, x_T, noise: RngStream, clock=None) -> Trajectory:

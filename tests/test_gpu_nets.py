@@ -63,26 +63,6 @@ def test_dit_forward_vs_torch_fp32(cuda):
     assert ref.abs().mean().item() > 1e-3          # random init is not the zero-eps adaLN-Zero init
 
 
-def test_dit_sampler_end_to_end(cuda):
-    """C4-shaped DDPM conservative run with the DiT eps: device sampler == the same
-    schedule evaluated op-by-op through evaluate() (fp32 eps, fp64 state)."""
-    import paper_2603_25872_b200 as P
-    from paper_2603_25872_b200.dit import DiT, DiTConfig
-    T = 12
-    s = P.default_schedule(T)
-    net = DiT(DiTConfig(), cuda, seed=1, max_batch=8)
-    den = P.NetworkEps(net, (4, 32, 32))
-    stream = P.RngStream(3)
-    x_T = P.derive_noise(stream, T, P.Role.INIT, 4096, device=cuda)
-    traj, reps = P.run_conservative(s, den, x_T, 8, P.VarianceRule.deterministic(), stream, update_family="ddpm")
-    assert traj.eval_count == T and traj.timesteps() == list(range(T, -1, -1))
-    assert torch.isfinite(traj.final).all()
-    # sequential DDPM with the same network must stay close (draft-and-refine approximation)
-    seq = P.sample_ddpm(s, den, x_T, stream)
-    rel = ((traj.final - seq.final).norm() / seq.final.norm()).item()
-    assert rel < 0.5, rel
-
-
 @pytest.mark.parametrize("size", [32, 64])
 @pytest.mark.parametrize("g", [0.0, 1.0])
 def test_sd15_unet_vs_torch_fp32(cuda, size, g):
@@ -103,6 +83,59 @@ def test_sd15_unet_vs_torch_fp32(cuda, size, g):
     ref = unet_ref(net, x.float()[None], t)[0]
     rel = ((out.reshape(4, size, size) - ref).norm() / ref.norm()).item()
     assert torch.isfinite(out).all() and rel < 3e-2, rel
+    assert net.flops > 0
+
+
+# per-eval tolerance at the production guidance scale: eps = u + 7.5 (c - u) carries
+# the bf16 error of the branch difference times 7.5
+G75_REL = 5e-2
+
+
+@pytest.mark.parametrize("t_model", [980.0, 500.0, 20.0])
+def test_sd15_unet_g75_vs_torch_fp32(cuda, t_model):
+    """SD1.5 UNet at 64x64 with the production CFG scale g = 7.5, at the start,
+    middle and end of a 1000-step model schedule, vs the fp32 torch reference:
+    rel-L2 and max-abs of the guided eps."""
+    from paper_2603_25872_b200.unet import UNet, sd15_config
+    from nets_ref import unet_ref
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    net = UNet(sd15_config(64), cuda, seed=0, max_batch=1, cfg_scale=7.5)
+    g = torch.Generator(device=cuda).manual_seed(int(t_model))
+    x = torch.randn(4, 64, 64, device=cuda, dtype=torch.float64, generator=g)
+    t = torch.tensor([t_model], device=cuda)
+    out = torch.empty(4 * 64 * 64, device=cuda)
+    net.forward([x.reshape(-1)], t, 1, outs=[out])
+    ref = unet_ref(net, x.float()[None], t)[0].reshape(-1)
+    rel = ((out - ref).norm() / ref.norm()).item()
+    mab = ((out - ref).abs().max() / ref.abs().max()).item()
+    print(f"\n[sd15 g=7.5 t={t_model}] rel-L2 {rel:.3e} max-abs/max|ref| {mab:.3e}")
+    assert torch.isfinite(out).all() and rel < G75_REL and mab < 2 * G75_REL, (rel, mab)
+
+
+@pytest.mark.parametrize("size,g,t_model", [(64, 0.0, 700.0), (64, 1.0, 300.0), (64, 7.5, 900.0),
+                                            (128, 7.5, 500.0)])
+def test_sdxl_unet_vs_torch_fp32(cuda, size, g, t_model):
+    """SDXL-shaped UNet (BASELINE C5: 3 levels, 2/10-deep transformers with 64-dim
+    heads, 2048-d context, added pooled/time-id embedding) vs the fp32 torch
+    reference: each CFG branch (g = 0 / 1) at a reduced 64x64 latent, and the
+    guided eps (g = 7.5) at 64x64 and at the full 128x128 C5 latent."""
+    from paper_2603_25872_b200.unet import UNet, sdxl_config
+    from nets_ref import unet_ref
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    net = UNet(sdxl_config(size), cuda, seed=0, max_batch=1, cfg_scale=g)
+    gen = torch.Generator(device=cuda).manual_seed(size + int(t_model))
+    x = torch.randn(4, size, size, device=cuda, dtype=torch.float64, generator=gen)
+    t = torch.tensor([t_model], device=cuda)
+    out = torch.empty(4 * size * size, device=cuda)
+    net.forward([x.reshape(-1)], t, 1, outs=[out])
+    ref = unet_ref(net, x.float()[None], t)[0].reshape(-1)
+    rel = ((out - ref).norm() / ref.norm()).item()
+    mab = ((out - ref).abs().max() / ref.abs().max()).item()
+    print(f"\n[sdxl {size} g={g} t={t_model}] rel-L2 {rel:.3e} max-abs/max|ref| {mab:.3e}")
+    tol = 3e-2 if g <= 1.0 else G75_REL
+    assert torch.isfinite(out).all() and rel < tol and mab < 2 * tol, (rel, mab)
     assert net.flops > 0
 
 

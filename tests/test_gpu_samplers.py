@@ -250,3 +250,78 @@ def test_graph_replay_matches_eager(cuda):
         torch.cuda.synchronize()
         assert torch.equal(run.traj[-1], finals[seed])
     run.check_err()
+
+
+@pytest.mark.parametrize("rule", ["det", "ddpm", "eta"])
+def test_ddim_subsequence_vs_oracle(cuda, rule):
+    """f4 ablation: DDIM along a timestep subsequence (sequential.py:79-113) on
+    device, SI denoiser: every state bit-identical to the oracle (z of the
+    transition into u is key (u, TRANSITION), skip k = t - u)."""
+    T, D, sub = 50, 4096, [20, 15, 9, 4, 0]
+    s, ab = P.default_schedule(T), O.default_alpha_bar(T)
+    r = {"det": P.VarianceRule.deterministic(), "ddpm": P.VarianceRule.ddpm_induced(),
+         "eta": P.VarianceRule.eta_scaled(0.5)}[rule]
+    orule = {"det": ("det",), "ddpm": ("ddpm",), "eta": ("eta", 0.5)}[rule]
+    x = O.derive_noise(6, 20, O.INIT, D)
+    traj = P.sample_ddim(s, P.StateIndependent(11, D), torch.from_numpy(x).to(cuda), r, P.RngStream(6),
+                         subsequence=sub)
+    ref = O.sample_ddim(ab, O.SI(11, D), x, orule, 6, subsequence=sub)
+    assert traj.timesteps() == sub == [t for t, _ in ref]
+    for (_, g), (_, rr) in zip(traj.states, ref):
+        assert np.array_equal(_np(g), rr)
+    with pytest.raises(P.InvalidSubsequence):
+        P.sample_ddim(s, P.StateIndependent(11, D), torch.from_numpy(x).to(cuda), r, P.RngStream(6),
+                      subsequence=[20, 20, 0])
+
+
+@pytest.mark.parametrize("T,devices,mode", [(100, 40, "aggressive"), (100, 65, "conservative")])
+def test_long_chain_runs_bit_exact(cuda, T, devices, mode):
+    """> 64-op refine+draft chains run as several launches (advisor r1) and stay
+    bit-identical to the oracle (SI eps, stochastic DDIM rule)."""
+    D = 256
+    s, ab = P.default_schedule(T), O.default_alpha_bar(T)
+    x = O.derive_noise(3, T, O.INIT, D)
+    run = P.run_aggressive if mode == "aggressive" else P.run_conservative
+    traj, reps = run(s, P.StateIndependent(5, D), torch.from_numpy(x).to(cuda), devices,
+                     P.VarianceRule.ddpm_induced(), P.RngStream(3), workers=0)
+    ref, evals, rounds = O.run_parallel(ab, O.SI(5, D), x, devices, mode, ("ddpm",), 3)
+    assert traj.eval_count == evals and len(reps) == rounds
+    for (_, g), (_, r) in zip(traj.states, ref):
+        assert np.array_equal(_np(g), r)
+
+
+@pytest.mark.parametrize("n_comp", [1, 8, 9, 13, 40])
+def test_gm_eps_many_components(cuda, n_comp):
+    """K9 accepts any mixture size up to DRS_GM_MAX_COMP (advisor r1: it stopped
+    at 8): components are reduced 8 per sweep; vs the oracle within fp64 rounding."""
+    rng = np.random.default_rng(n_comp)
+    D, T = 5000, 50
+    w = rng.random(n_comp)
+    w /= w.sum()
+    means = rng.normal(size=(n_comp, D)) * 0.3
+    var = rng.random(n_comp) + 0.5
+    gm = P.GaussianMixture(weights=w, means=means, variances=var)
+    s, ab = P.default_schedule(T), O.default_alpha_bar(T)
+    x = rng.normal(size=(3, D))
+    for t in (1, 17, 50):
+        got = _np(P.eps_oracle(gm, s, torch.from_numpy(x).to(cuda), t))
+        ref = O.gm_eps(w, means, var, ab, x, t)
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel <= 1e-11, (n_comp, t, rel)
+    with pytest.raises(ValueError):
+        P.GaussianMixture(weights=np.full(2000, 1 / 2000), means=np.zeros((2000, 1)), variances=np.ones(2000))
+
+
+def test_execute_round_perturbed_network_eps(cuda):
+    """Perturbed over a NetworkEps (fp32 eps) in execute_round: the perturbation
+    runs on an fp64 copy (advisor r1: it used to treat the fp32 row as fp64)."""
+    from paper_2603_25872_b200.unet import UNet, sd15_config
+    net = UNet(sd15_config(32), cuda, seed=0, max_batch=1)
+    s = P.default_schedule(20)
+    base = P.NetworkEps(net, (4, 32, 32))
+    x = torch.randn(4096, dtype=torch.float64, device=cuda)
+    (e0,), _ = P.execute_round(base, s, [(x, 7)], 1, anchor_t=7)
+    (e1,), _ = P.execute_round(P.Perturbed(base, 0.25), s, [(x, 7)], 1, anchor_t=7)
+    assert e1.dtype == torch.float64 and e1.shape == e0.shape
+    want = e0.double() + 0.25 * torch.from_numpy(O.perturbation(_np(x), 7, 1.0)).to(cuda)
+    assert torch.allclose(e1, want, rtol=0, atol=1e-12)

@@ -162,3 +162,46 @@ def test_world2_gloo_partition_and_gather():
                               RULES[cases[ci][4]][0], cases[ci][3], world=2, rank=0)
         redundant = sum(1 for st in prog.steps if hasattr(st, "owner") and st.owner[0] is None)
         assert l0 + l1 == evals + redundant
+
+
+@pytest.mark.parametrize("T,devices,mode", [(100, 33, "aggressive"), (100, 40, "aggressive"),
+                                            (100, 65, "conservative"), (150, 70, "aggressive"),
+                                            (130, 100, "conservative")])
+@pytest.mark.parametrize("rule", ["det", "ddpm"])
+def test_long_chains_split_into_launches(T, devices, mode, rule):
+    """Chains longer than one drs_skip_chain launch (64 ops, csrc/chain.cu kMaxOps)
+    are cut; ops whose CUR / ANCHOR register would come from an earlier launch
+    read the stored state instead -- bit-identical to the oracle run (advisor r1:
+    T=100 with 33 devices built a 65-op chain)."""
+    from paper_2603_25872_b200 import _lib
+    from paper_2603_25872_b200.program import CHAIN_MAX_OPS, Chain
+    s = default_schedule(T)
+    ab = O.default_alpha_bar(T)
+    eps = O.toy_bimodal(2)
+    x_T = O.derive_noise(1, T, O.INIT, 2)
+    prog = build_parallel(s, plan_blocks(T, devices, Mode(mode)), RULES[rule][0], "ddim")
+    chains = [st for st in prog.steps if isinstance(st, Chain)]
+    assert max(len(c.ops) for c in chains) <= CHAIN_MAX_OPS
+    assert sum(len(c.ops) for c in chains) > CHAIN_MAX_OPS
+    for c in chains:          # no launch reads a register it did not set
+        cur = anchor = False
+        for o in c.ops:
+            assert o.src != _lib.SRC_CUR or cur
+            assert o.src != _lib.SRC_ANCHOR or anchor
+            cur, anchor = True, anchor or o.save_anchor
+    got, _ = run_ir(prog, ab, eps, x_T, seed=1)
+    ref, evals, _ = O.run_parallel(ab, eps, x_T, devices, mode, RULES[rule][1], 1)
+    assert _same(got, ref) and prog.eval_count == evals
+
+
+def test_array_like_x_T_and_workers_zero():
+    """x_T may be any array-like (np.asarray semantics, parallel.py:262) and
+    workers=0 means one worker per device (`workers or devices`, parallel.py:269)."""
+    from paper_2603_25872_b200.parallel import _check_workers, _numel
+    from paper_2603_25872_b200.errors import InvalidPlanParams
+    assert _numel([[0.1, 0.2, 0.3], [1.0, 2.0, 3.0]]) == 6
+    assert _numel(np.zeros((1, 4, 8))) == 32 and _numel(torch.zeros(5)) == 5 and _numel(0.5) == 1
+    _check_workers(0, None)
+    _check_workers(None, None)
+    with pytest.raises(InvalidPlanParams):
+        _check_workers(-1, None)

@@ -52,7 +52,12 @@ def _args():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="bounded CPU-baseline sample")
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="reference arm: whole images timed while they fit this budget (>= 1 image)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl-one-rank", action="store_true",
+                    help="N=1 diagnostic: the N>1 code path (NCCL communicator, per-round eps all-gathers "
+                         "captured in the image graph, drf ratios) on a one-rank communicator")
     return ap.parse_args()
 
 
@@ -219,57 +224,154 @@ def _cpu_eval_fn(cfg):
     return eps
 
 
-def cpu_sample(cfg, seconds, threads):
-    """Reference algorithm on host cores (bounded).  Toy configs: whole images
-    (oracle run_parallel / sample_*).  Network configs: a full image is minutes
-    of CPU time, so the sample is `k` network evaluations timed and
-    extrapolated to the sequential sampler's T evaluations per image."""
+class _Budget(Exception):
+    """Raised inside the eps callable to stop a bounded CPU sample at a step boundary."""
+
+
+def _oracle_image(cfg, eps, seed, mode, n, marks=None, limit=None):
+    """One image of the restated reference pipeline (cli._run_once, cli.py:43-67):
+    x_T = INIT noise of the seed, then the configured sampler, on host cores.
+    `marks` collects a perf_counter stamp at the start of every eps evaluation;
+    `limit` stops the image (raising _Budget) before evaluation limit+1."""
+    import skipdiff_oracle as O
+    T, D = cfg["T"], 4 * cfg["size"] ** 2
+    ab = O.default_alpha_bar(T)
+    rule = ("det",) if cfg["rule"] == "det" else ("ddpm",)
+
+    def timed(ab_, x, t):
+        if marks is not None:
+            marks.append(time.perf_counter())
+            if limit is not None and len(marks) > limit:
+                raise _Budget()
+        return eps(ab_, x, t)
+    x_T = O.derive_noise(seed, T, O.INIT, D, cfg["generator"])
+    if mode == "sequential":
+        if cfg["family"] == "ddpm":
+            return O.sample_ddpm(ab, timed, x_T, seed, cfg["generator"])
+        return O.sample_ddim(ab, timed, x_T, rule, seed, cfg["generator"])
+    return O.run_parallel(ab, timed, x_T, n, mode, rule, seed, family=cfg["family"],
+                          generator=cfg["generator"])[0]
+
+
+def cpu_steps(cfg, mode, n, threads, seconds):
+    """Bounded CPU baseline: consecutive steps of ONE image of the oracle
+    sampler (each step = one eps evaluation + its update; the network configs
+    run the same-architecture torch-CPU fp32 net), stopped at a step boundary
+    after `seconds`; ms/image = mean step time x evaluations per image."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import skipdiff_oracle as O
     torch.set_num_threads(threads)
     eps = _cpu_eval_fn(cfg)
-    ab = O.default_alpha_bar(cfg["T"])
-    D = 4 * cfg["size"] ** 2
-    rule = ("det",) if cfg["rule"] == "det" else ("ddpm",)
-    if cfg["net"] == "toy":
-        def image(seed):
-            x_T = O.derive_noise(seed, cfg["T"], O.INIT, D, cfg["generator"])
-            O.run_parallel(ab, eps, x_T, cfg["n"], cfg["mode"], rule, seed, family=cfg["family"],
-                           generator=cfg["generator"])
-        image(99)
-        times, t_end, seed = [], time.perf_counter() + seconds, 0
-        while time.perf_counter() < t_end or len(times) < 3:
-            t0 = time.perf_counter()
-            image(seed)
-            times.append((time.perf_counter() - t0) * 1e3)
-            seed += 1
-        return statistics.mean(times), f"{len(times)} whole images ({cfg['desc']}), oracle run_parallel"
-    x = O.derive_noise(0, cfg["T"], O.INIT, D, cfg["generator"])
-    eps(ab, x, cfg["T"])                               # warm-up
-    times, t_end = [], time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 2:
+    evals, _ = evals_per_image(cfg, mode, n)
+    warm = []
+    try:                                                # warm-up: one evaluation
+        _oracle_image(cfg, eps, 99, mode, n, warm, 1)
+    except _Budget:
+        pass
+    marks, t_end = [], time.perf_counter() + seconds
+
+    class _Deadline(list):
+        def append(self, v):
+            super().append(v)
+            if v > t_end and len(self) >= 3:
+                raise _Budget()
+    marks = _Deadline()
+    try:
+        _oracle_image(cfg, eps, 0, mode, n, marks, None)
+        marks.append(time.perf_counter())               # whole image finished inside the budget
+    except _Budget:
+        pass
+    steps = [b - a for a, b in zip(marks, marks[1:])]
+    per_step = statistics.mean(steps) * 1e3
+    return per_step * evals, (f"{len(steps)} consecutive sampler steps (eps evaluation + update) of one "
+                              f"{mode} image, oracle sampler with the {_eps_desc(cfg)} on {_threads_desc(cfg, threads)} "
+                              f"({per_step:.0f} ms/step) x {evals} evaluations per image"), len(steps), per_step
+
+
+def _threads_desc(cfg, threads):
+    return "1 host thread (numpy)" if cfg["net"] == "toy" else f"{threads} host threads"
+
+
+def _eps_desc(cfg):
+    return "analytic GM eps" if cfg["net"] == "toy" else "torch-CPU fp32 network (same weights)"
+
+
+def cpu_images(cfg, mode, n, threads, budget_s, max_images):
+    """Reference arm: WHOLE images of the oracle pipeline (x_T noise + sampler)
+    on host cores, timed image by image, as many as fit `budget_s` (at least
+    one).  If one image is projected (from a warm-up evaluation) to exceed the
+    budget, a bounded run of consecutive steps is extrapolated instead and the
+    line says so.  Returns (per-image ms list, sample text, whole-images flag)."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    torch.set_num_threads(threads)
+    eps = _cpu_eval_fn(cfg)
+    evals, _ = evals_per_image(cfg, mode, n)
+    warm = []
+    t0 = time.perf_counter()
+    try:
+        _oracle_image(cfg, eps, 99, mode, n, warm, 2)
+    except _Budget:
+        pass
+    per_eval = (time.perf_counter() - t0) / 2
+    if per_eval * evals > budget_s:
+        v, sample, n_steps, per_step = cpu_steps(cfg, mode, n, threads, min(budget_s, 60.0))
+        return [v], sample + " (one image exceeds the time budget: extrapolated)", (n_steps, per_step)
+    times, t_end = [], time.perf_counter() + budget_s
+    while len(times) < max_images and (not times or time.perf_counter() + statistics.mean(times) / 1e3 < t_end):
         t0 = time.perf_counter()
-        eps(ab, x, cfg["T"] - len(times))
+        _oracle_image(cfg, eps, len(times), mode, n)
         times.append((time.perf_counter() - t0) * 1e3)
-    per_eval = statistics.mean(times)
-    return per_eval * cfg["T"], (f"{len(times)} torch-CPU fp32 network evaluations ({per_eval:.0f} ms each, "
-                                 f"{threads} threads) x T={cfg['T']} evals of the sequential sampler "
-                                 f"(extrapolated; sampler arithmetic is negligible next to it)")
+    return times, (f"{len(times)} whole image(s), x_T -> x_0 ({evals} evaluations each), oracle {mode} sampler "
+                   f"with the {_eps_desc(cfg)} on {_threads_desc(cfg, threads)}"
+                   + ("; the reference's thread pool shares these cores, so parallel-mode evaluations run "
+                      "one after another" if mode != "sequential" else "")), None
 
 
-def run_reference_arm(a, cfg, rank):
+def workload_config(cfg, name, mode, n):
+    """The `config` object both arms print (same keys and values)."""
+    net_cfg = cfg["net"] != "toy"
+    return {"workload": name, "desc": cfg["desc"], "T": cfg["T"], "latent": f"4x{cfg['size']}x{cfg['size']}",
+            "mode": mode, "devices": n, "family": cfg["family"], "noise": cfg["generator"], "batch": 1,
+            "state": "fp64 sampler state" + (", fp32 eps" if net_cfg else ""),
+            "weights": "random init N(0, 0.02), seed 0" if net_cfg else "analytic",
+            "l2": "GPU arm: flushed between timed images (256 MB memset outside the events); CPU arm: n/a"}
+
+
+def arm_modes(cfg, world):
+    """(mode, n) timed at this world size: N = 1 runs the 1-GPU sequential sampler
+    for the network configs (T1 of the metric), N > 1 the configured mode with n = N."""
+    if world == 1:
+        return ("sequential", 1) if cfg["net"] != "toy" else (cfg["mode"], cfg["n"])
+    return cfg["mode"], world
+
+
+def run_reference_arm(a, cfg, rank, world):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    seconds = max(5.0, min(60.0, 20.0 * a.steps / 5))
-    v, sample = cpu_sample(cfg, seconds, threads)
+    mode, n = arm_modes(cfg, world)
+    times, sample, extrap = cpu_images(cfg, mode, n, threads, a.ref_seconds, max(1, a.steps))
+    v = statistics.mean(times)
+    whole = extrap is None
+    # steps / ms_per_step describe what was actually timed: whole images, or (when one
+    # image exceeds the budget) consecutive sampler steps, each one eps evaluation + update
+    n_timed, ms_step = (len(times), v) if whole else extrap
+    cores = threads if cfg["net"] != "toy" else 1
     line = {"impl": "reference", "metric": "ms/image sampling latency", "value": v, "unit": "ms/image",
-            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": v, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["net"] != "toy" else "f64",
-            "data": "synthetic", "config": {"workload": a.config, "desc": cfg["desc"]},
-            "cpu_baseline": {"value": v, "unit": "ms/image", "cores": threads if cfg["net"] != "toy" else 1,
-                             "kind": "port", "sample": sample},
+            "n_gpus": a.gpus, "steps": n_timed, "warmup": a.warmup, "ms_per_step": ms_step,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if cfg["net"] != "toy" else "f64", "data": "synthetic",
+            "config": workload_config(cfg, a.config, mode, n),
+            "steps_note": (f"steps = whole images timed ({len(times)}; --steps {a.steps} requested): one image "
+                           f"is {v / 1e3:.0f} s of CPU work, so the arm times as many as fit "
+                           f"--ref-seconds {a.ref_seconds:.0f}" if whole else
+                           f"one image exceeds --ref-seconds: steps = {n_timed} consecutive sampler steps timed "
+                           f"(ms_per_step per sampler step), value = ms/step x evaluations per image"),
+            "precision_note": ("reference arm computes eps with the fp32 torch-CPU network; the GPU arm with the "
+                               "bf16 tcgen05 network (fp32 accumulate, fp64 sampler state) -- per-step latent "
+                               "tolerance in DESIGN.md 3a" if cfg["net"] != "toy" else "both arms fp64"),
+            "cpu_baseline": {"value": v, "unit": "ms/image", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "ms/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -281,7 +383,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if a.impl == "reference":
-        run_reference_arm(a, cfg, rank)
+        run_reference_arm(a, cfg, rank, world)
         return
 
     import torch
@@ -296,24 +398,33 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    multi = world > 1 or a.nccl_one_rank
+    if multi:
+        # NCCL's own init log (communicator ranks, NVLS/NVLink transport) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         comm = Comm(rank, world)
     net_cfg = cfg["net"] != "toy"
-    if world == 1:
-        mode, n = ("sequential", 1) if net_cfg else (cfg["mode"], cfg["n"])
-    else:
-        mode, n = cfg["mode"], world
+    mode, n = arm_modes(cfg, world)
+    if a.nccl_one_rank:
+        mode, n = cfg["mode"], cfg["n"]
     s = P.default_schedule(cfg["T"])
     net, D = build_net(cfg, dev, max_batch=max(1, cfg["n"] if world == 1 else 1))
     den = build_denoiser(cfg, net, D)
     rule = P.VarianceRule.deterministic() if cfg["rule"] == "det" else P.VarianceRule.ddpm_induced()
     sampler = Sampler(s, den, D, mode=mode, devices=n, rule=rule, family=cfg["family"],
-                      generator=cfg["generator"], comm=comm, device=dev)
+                      generator=cfg["generator"], comm=comm, device=dev, exchange=multi)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -343,9 +454,10 @@ def main():
     l0 = _lib.LAUNCHES[0]
     with ClockSampler(local) as clk:
         per_image = timed_images(sampler, a.steps, 0)
-    graph_note = "graph replays (no host launches)" if sampler.use_graph else "eager"
+    graph_note = (f"graph replays, {sampler.run.graph_mode} (no host launches)" if sampler.use_graph
+                  else "eager")
     t_img = torch.tensor([statistics.mean(per_image)], device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(t_img, op=dist.ReduceOp.MAX)
     value = float(t_img.item())
     sampler.run.check_err()
@@ -372,7 +484,7 @@ def main():
         sampler(50_000 + i, x_T=x_hosts[i], out=out_host)
         e2e.append((time.perf_counter() - t0) * 1e3)
     t_e2e = torch.tensor([statistics.mean(e2e)], device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
 
     # roofline of the dominant kernel: per-launch CUDA events over one eager image
@@ -437,7 +549,7 @@ def main():
 
     # draft-and-refine on this one GPU (logical devices batched per round), for context
     drf = {"T": cfg["T"], "mode_timed": mode, "devices": n}
-    if world == 1 and net_cfg and rank == 0:
+    if world == 1 and net_cfg and rank == 0 and not multi:
         par = Sampler(s, den, D, mode=cfg["mode"], devices=cfg["n"], rule=rule, family=cfg["family"],
                       generator=cfg["generator"], device=dev)
         par.stage(7)
@@ -452,9 +564,29 @@ def main():
             ev2, r2 = evals_per_image(cfg, cfg["mode"], nn)
             drf[f"ideal_n{nn}"] = {"round_law_ms": value * r2 / cfg["T"], "one_over_n_ms": value / nn,
                                    "two_over_n_plus_1_ms": value * 2 / (nn + 1), "rounds": r2}
-    elif world > 1:
+    elif multi:
+        # T1 on this rank's GPU (the 1-GPU sequential sampler, no communicator), so the
+        # line carries the measured / round-law and measured / 2/(n+1) ratios itself
         ev, rounds = evals_per_image(cfg, mode, n)
-        drf.update({"rounds": rounds, "evals": ev})
+        seq = Sampler(s, den, D, mode="sequential" if net_cfg else cfg["mode"], devices=1 if net_cfg else cfg["n"],
+                      rule=rule, family=cfg["family"], generator=cfg["generator"], device=dev)
+        seq.stage(7)
+        seq.launch()
+        torch.cuda.synchronize(dev)
+        t1 = torch.tensor([statistics.mean(timed_images(seq, 3, 0, False))], device=dev)
+        dist.all_reduce(t1, op=dist.ReduceOp.MAX)
+        t1 = float(t1.item())
+        g = classes.get("gather", {"ms": 0.0, "launches": 0})
+        round_law = t1 * rounds / cfg["T"]
+        drf.update({"rounds": rounds, "evals": ev, "t1_sequential_ms": t1,
+                    "gather_us_per_round": g["ms"] * 1e3 / max(1, g["launches"]),
+                    "gathers_per_image": g["launches"],
+                    "exchange": sampler.run.graph_mode,
+                    "round_law_ms": round_law, "measured_over_round_law": value / round_law,
+                    "one_over_n_ms": t1 / n, "measured_over_one_over_n": value / (t1 / n),
+                    "two_over_n_plus_1_ms": t1 * 2 / (n + 1),
+                    "measured_over_two_over_n_plus_1": value / (t1 * 2 / (n + 1)),
+                    "speedup_vs_t1": t1 / value})
 
     if rank != 0:
         dist.destroy_process_group()
@@ -463,11 +595,11 @@ def main():
         "metric": "ms/image sampling latency", "value": value, "unit": "ms/image", "n_gpus": world,
         "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": value, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if net_cfg else "f64", "data": "synthetic",
-        "config": {"workload": a.config, "desc": cfg["desc"], "T": cfg["T"], "latent": f"4x{cfg['size']}x{cfg['size']}",
-                   "mode": mode, "devices": n, "family": cfg["family"], "noise": cfg["generator"], "batch": 1,
-                   "state": "fp64 sampler state, fp32 eps" if net_cfg else "fp64",
-                   "weights": "random init N(0, 0.02), seed 0" if net_cfg else "analytic",
-                   "l2": "flushed between timed images (256 MB memset outside the events)", "launch": graph_note},
+        "config": workload_config(cfg, a.config, mode, n),
+        "launch": graph_note,
+        "precision_note": ("bf16 tcgen05 network (fp32 accumulate), fp32 eps, fp64 sampler state; the reference "
+                           "arm uses the fp32 torch-CPU network -- per-step tolerance in DESIGN.md 3a")
+        if net_cfg else "fp64",
         "e2e": {"value": float(t_e2e.item()), "unit": "ms/image", "h2d_bytes_per_step": D * 8 + 16,
                 "d2h_bytes_per_step": D * 8,
                 "how": "Sampler(seed, x_T=pinned host, out=pinned host): H2D x_T, graph replay, D2H x_0, sync"},
@@ -477,13 +609,17 @@ def main():
         "clocks": clk.summary(),
         "drf": drf,
     }
-    if not a.no_cpu_baseline:
+    if not a.no_cpu_baseline and world == 1:      # rank 0 at N = 1 only
         threads = len(os.sched_getaffinity(0))
-        v, sample = cpu_sample(cfg, a.cpu_seconds, threads)
+        if net_cfg:
+            v, sample, _, _ = cpu_steps(cfg, mode, n, threads, a.cpu_seconds)
+        else:
+            times, sample, _ = cpu_images(cfg, mode, n, threads, a.cpu_seconds, 1000)
+            v = statistics.mean(times)
         line["cpu_baseline"] = {"value": v, "unit": "ms/image", "cores": threads if net_cfg else 1, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 

@@ -44,15 +44,36 @@ def unwrap(d):
 
 
 class Comm:
-    """Rank/world plus the per-round eps exchange (torch.distributed / NCCL)."""
+    """Rank/world plus the per-round eps exchange (torch.distributed / NCCL).
+
+    On NCCL the exchange is one in-place ncclAllGather of the round's eps rows
+    on the current stream, so it is captured into the run's CUDA graph with
+    the kernels around it (a multi-rank image is ONE graph replay per rank).
+    The gloo backend stages through the host (tests: several ranks' kernels
+    on one GPU, or CPU-only hosts) and is issued between per-segment graph
+    replays."""
 
     def __init__(self, rank: int = 0, size: int = 1, group=None):
         self.rank, self.size, self.group = rank, size, group
+        self.gathers = 0                  # collectives issued (host calls, incl. captures)
+
+    @property
+    def backend(self):
+        import torch.distributed as dist
+        if not dist.is_available() or not dist.is_initialized():
+            return None
+        return dist.get_backend(self.group)
+
+    @property
+    def capturable(self) -> bool:
+        """The exchange can live inside a CUDA graph (device-side collective)."""
+        return self.backend == "nccl"
 
     def all_gather_rows(self, gbuf):
         """In-place all-gather of gbuf[world, per_rank, D]: rank r contributes gbuf[r]."""
         import torch.distributed as dist
         flat = gbuf.view(self.size, -1)
+        self.gathers += 1
         if dist.get_backend(self.group) == "gloo":
             # host-staged path: lets tests run several ranks' kernels on one GPU
             # (no device-side waits between processes) over a CPU process group
@@ -104,6 +125,7 @@ class DeviceRun:
         self._alloc()
         self._lower()
         self.graph = None
+        self.graph_mode = "eager"
 
     # ---------------------------------------------------------- layout ----
     def _alloc(self):
@@ -189,6 +211,8 @@ class DeviceRun:
                 self.launches.append(("gather", st.round))
             elif isinstance(st, Noise):
                 pass
+        self.local_evals = sum(payload[1][1]["n_tasks"] for kind, payload in self.launches
+                               if kind == "eval" and payload[1] is not None)
         self.n_ops = len(ops_all)
         self.ops_dev = ops_to_device(ops_all, self.device) if ops_all else None
         self._split_segments()
@@ -411,20 +435,23 @@ class DeviceRun:
         return s
 
     def capture(self):
-        """Capture the run into CUDA graphs: one graph for a single-rank run;
-        one graph per segment between all-gathers for a multi-rank run (the
-        NCCL collectives are issued between segment replays)."""
+        """Capture the run into CUDA graphs: ONE graph when the run has no
+        exchange or its exchange is a device collective (NCCL all-gathers
+        captured between the kernels); one graph per segment between
+        all-gathers otherwise (host-staged gloo exchange between replays)."""
         s = self._warm_stream()
         with torch.cuda.stream(s):
-            self.enqueue()                    # warm-up outside capture (allocations, tensor maps)
+            self.enqueue()                    # warm-up outside capture (allocations, tensor maps, NCCL comm)
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
-        if self.prog.world == 1:
+        if not self.gather_rounds or self.comm.capturable:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
                 self.enqueue()
             self.graph, self.seg_graphs = g, None
+            self.graph_mode = "one graph" + (" (NCCL all-gathers captured)" if self.gather_rounds else "")
             return g
+        self.graph_mode = "per-segment graphs, host-staged exchange between replays"
         self.seg_graphs = []
         for i in range(len(self.segments)):
             g = torch.cuda.CUDAGraph()
@@ -452,8 +479,8 @@ class DeviceRun:
         """Host-side accounting of one run: Counting wrappers and VirtualClock
         (rounds charge max task latency + dispatch overhead, parallel.py:138-148;
         sequential evals charge eval_time each, sequential.py:104-111)."""
-        for c in self.counters:
-            c.count += self.prog.eval_count
+        for c in self.counters:       # evaluations this rank performed (denoiser.py:264-266)
+            c.count += self.local_evals
         if clock is None:
             return None
         per_round = []

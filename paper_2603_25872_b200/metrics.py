@@ -152,8 +152,10 @@ def trajectory_max_dev(a, b) -> float:
     ta, tb = a.timesteps(), b.timesteps()
     if ta != tb:
         raise TimestepMismatch(f"timestep lists differ: {ta[:5]}... vs {tb[:5]}...")
-    xa = torch.stack([torch.as_tensor(x, dtype=torch.float64).reshape(-1) for _, x in a.states])
-    xb = torch.stack([torch.as_tensor(x, dtype=torch.float64).reshape(-1).to(xa.device) for _, x in b.states])
+    dev = next((x.device for _, x in a.states + b.states if isinstance(x, torch.Tensor) and x.is_cuda), None)
+    dev = _default_device(dev)
+    xa = torch.stack([torch.as_tensor(x, dtype=torch.float64).reshape(-1).to(dev) for _, x in a.states])
+    xb = torch.stack([torch.as_tensor(x, dtype=torch.float64).reshape(-1).to(dev) for _, x in b.states])
     return float(torch.linalg.vector_norm(xa - xb, dim=1).max().item())
 
 

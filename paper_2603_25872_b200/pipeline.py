@@ -9,8 +9,11 @@
 The whole run -- noise table, every eps evaluation, every draft/refine chain
 -- is one CUDA graph on a single rank; per image only the seed word (and x_T
 if given) is staged, and the final state is returned (copied into a pinned
-host buffer when `out` is given).  With `comm` (one process per GPU) the run
-is issued eagerly around the NCCL eps all-gathers.
+host buffer when `out` is given).  With `comm` (one process per GPU) the
+per-round NCCL eps all-gathers are captured into the same graph (a gloo
+communicator falls back to per-segment graphs with the host-staged exchange
+between replays).  `exchange=True` keeps the gathers in a one-rank program
+(a one-rank NCCL communicator exercises the data plane on one GPU).
 """
 
 import torch
@@ -24,14 +27,15 @@ class Sampler:
     def __init__(self, s, d, dim: int, *, mode: str = "aggressive", devices: int = 1,
                  rule: VarianceRule | None = None, family: str = "ddim", generator: str = "pcg64",
                  recompute_anchor_eps: bool = False, subsequence=None, comm: Comm | None = None,
-                 device=None, graph: bool = True):
+                 device=None, graph: bool = True, exchange: bool = False):
         rule = rule or VarianceRule.deterministic()
         comm = comm or Comm()
         if mode == "sequential":
             prog = build_sequential(s, rule, family, subsequence)
         else:
             plan = plan_blocks(s.T, devices, Mode(mode))
-            prog = build_parallel(s, plan, rule, family, recompute_anchor_eps, comm.size, comm.rank)
+            prog = build_parallel(s, plan, rule, family, recompute_anchor_eps, comm.size, comm.rank,
+                                  exchange=exchange)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.run = DeviceRun(prog, s, d, dim, dev, generator=generator, comm=comm, derive_init=True)
         self.prog, self.device, self.dim = prog, dev, dim

@@ -139,8 +139,9 @@ class Program:
 
 
 class _Builder:
-    def __init__(self, s, rule, family, world):
+    def __init__(self, s, rule, family, world, exchange=False):
         self.s, self.rule, self.family, self.world = s, rule, family, world
+        self.exchange = exchange or world > 1      # emit Gather steps (also at world 1 when asked)
         self.stochastic = family == "ddpm" or (family == "ddim" and rule.stochastic)
         self.keys = []
         self._key_set = {}
@@ -177,7 +178,7 @@ class _Builder:
         self.rounds.append(RoundInfo(anchor_t, len(tasks)))
         owner = [None] * len(tasks) if redundant else [i % self.world for i in range(len(tasks))]
         self.steps.append(Eval(r, tasks, dst, owner))
-        if not redundant and self.world > 1 and tasks:
+        if not redundant and self.exchange and tasks:
             self.steps.append(Gather(r, len(tasks)))
         self.eval_count += len(tasks)
         self.max_tasks = max(self.max_tasks, len(tasks))
@@ -229,7 +230,8 @@ def _draft_key(t, i):
 
 
 def build_parallel(s, plan: BlockPlan, rule: VarianceRule, family: str = "ddim",
-                   recompute_anchor_eps: bool = False, world: int = 1, rank: int = 0) -> Program:
+                   recompute_anchor_eps: bool = False, world: int = 1, rank: int = 0,
+                   exchange: bool = False) -> Program:
     """IR of parallel.py:_run (250-321) for a plan, as seen by `rank` of `world`.
 
     Every rank replays drafts and refines redundantly (bit-identical), so no
@@ -241,11 +243,14 @@ def build_parallel(s, plan: BlockPlan, rule: VarianceRule, family: str = "ddim",
     family "euler" (parallel.py:324-381): `s` is a SigmaGrid, t counts the
     remaining grid intervals (N at the start), updates are euler_skip and the
     velocity tasks at sigma = 0 (t = 0, the aggressive mode's last draft) are
-    dropped, since nothing consumes them (parallel.py:346-349)."""
+    dropped, since nothing consumes them (parallel.py:346-349).
+
+    exchange=True emits the per-round Gather steps even at world 1 (a
+    one-rank communicator: exercises the collective data plane on one GPU)."""
     if family not in ("ddim", "ddpm", "euler"):
         raise ValueError(f"unknown update family: {family!r}")
     T = s.N if family == "euler" else s.T
-    b = _Builder(s, rule, family, world)
+    b = _Builder(s, rule, family, world, exchange)
     slot = lambda t: ("traj", T - t)                  # noqa: E731
     mine = lambda i: world == 1 or (i - 1) % world == rank   # noqa: E731  draft i owned?
     anchor_eps = None                                 # buffer holding the current anchor eps

@@ -82,17 +82,23 @@ def test_sd15_unet_vs_torch_fp32(cuda, size, g):
     net.forward([x.reshape(-1)], t, 1, outs=[out])
     ref = unet_ref(net, x.float()[None], t)[0]
     rel = ((out.reshape(4, size, size) - ref).norm() / ref.norm()).item()
+    print(f"\n[sd15 {size} g={g} t=601] rel-L2 {rel:.3e}")
     assert torch.isfinite(out).all() and rel < 3e-2, rel
     assert net.flops > 0
 
 
-# per-eval tolerance at the production guidance scale: eps = u + 7.5 (c - u) carries
-# the bf16 error of the branch difference times 7.5
-G75_REL = 5e-2
+# per-eval tolerance at the production guidance scale.  eps = u + 7.5 (c - u)
+# carries 7.5x the error of the branch difference: measured per-branch rel-L2 1.4e-2 (bf16
+# activations, test above), |c - u| / |u| = 5.2e-2 for this random-init net, so the
+# uncorrelated branch errors give ~7.5 * sqrt(2) * 1.4e-2 / |u + 7.5 (c - u)| / |u| ~ 0.14;
+# measured 0.118-0.124 (fold on / off alike).  SDXL's branches differ more (pooled text and
+# time ids per branch), so its guided error is 2.9e-2.
+G75_REL = 0.2
 
 
+@pytest.mark.parametrize("fold", [True, False])
 @pytest.mark.parametrize("t_model", [980.0, 500.0, 20.0])
-def test_sd15_unet_g75_vs_torch_fp32(cuda, t_model):
+def test_sd15_unet_g75_vs_torch_fp32(cuda, t_model, fold):
     """SD1.5 UNet at 64x64 with the production CFG scale g = 7.5, at the start,
     middle and end of a 1000-step model schedule, vs the fp32 torch reference:
     rel-L2 and max-abs of the guided eps."""
@@ -101,6 +107,7 @@ def test_sd15_unet_g75_vs_torch_fp32(cuda, t_model):
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     net = UNet(sd15_config(64), cuda, seed=0, max_batch=1, cfg_scale=7.5)
+    net.fold_cross = fold
     g = torch.Generator(device=cuda).manual_seed(int(t_model))
     x = torch.randn(4, 64, 64, device=cuda, dtype=torch.float64, generator=g)
     t = torch.tensor([t_model], device=cuda)
@@ -109,7 +116,13 @@ def test_sd15_unet_g75_vs_torch_fp32(cuda, t_model):
     ref = unet_ref(net, x.float()[None], t)[0].reshape(-1)
     rel = ((out - ref).norm() / ref.norm()).item()
     mab = ((out - ref).abs().max() / ref.abs().max()).item()
-    print(f"\n[sd15 g=7.5 t={t_model}] rel-L2 {rel:.3e} max-abs/max|ref| {mab:.3e}")
+    net.cfg_scale = 0.0
+    u = unet_ref(net, x.float()[None], t)[0].reshape(-1)
+    net.cfg_scale = 1.0
+    c = unet_ref(net, x.float()[None], t)[0].reshape(-1)
+    net.cfg_scale = 7.5
+    print(f"\n[sd15 g=7.5 t={t_model} fold={fold}] rel-L2 {rel:.3e} max-abs/max|ref| {mab:.3e} "
+          f"|c-u|/|u| {((c - u).norm() / u.norm()).item():.3e}")
     assert torch.isfinite(out).all() and rel < G75_REL and mab < 2 * G75_REL, (rel, mab)
 
 
@@ -134,7 +147,7 @@ def test_sdxl_unet_vs_torch_fp32(cuda, size, g, t_model):
     rel = ((out - ref).norm() / ref.norm()).item()
     mab = ((out - ref).abs().max() / ref.abs().max()).item()
     print(f"\n[sdxl {size} g={g} t={t_model}] rel-L2 {rel:.3e} max-abs/max|ref| {mab:.3e}")
-    tol = 3e-2 if g <= 1.0 else G75_REL
+    tol = 3e-2 if g <= 1.0 else 6e-2
     assert torch.isfinite(out).all() and rel < tol and mab < 2 * tol, (rel, mab)
     assert net.flops > 0
 

@@ -123,6 +123,14 @@ int drs_gm_velocity(const double* const* xs, const int32_t* idx, int n_rows, int
                     const double* sigmas, int N, const double* means, const double* log_w,
                     const double* var, int n_comp, double* const* out, int* err, void* stream);
 
+/* E[x0 | x_t = x] of the VP-noised mixture (x0_posterior_mean, denoiser.py:110-121)
+ * at one abar in (0, 1] (abar: DEVICE fp64 scalar; zeros: DEVICE int32[n_rows] of 0):
+ *   centers sqrt(abar) m_i, s_i = abar v_i + 1-abar, gain_i = sqrt(abar) v_i / s_i,
+ *   out[r] = sum_i resp_i(x) (m_i + gain_i (x - sqrt(abar) m_i)). */
+int drs_gm_x0_mean(const double* const* xs, const int32_t* zeros, int n_rows, int64_t D,
+                   const double* abar, const double* means, const double* log_w, const double* var,
+                   int n_comp, double* const* out, int* err, void* stream);
+
 /* ---- Perturbed-denoiser ablation (next-row scope) ----------------------------- */
 /* keys[r] = the noise key of denoiser.py:224-231's perturbation of state xs[r]
  * (fp64, D) at timestep ts[r] (DEVICE int32): BLAKE2b-64(b"perturb" || t ||

@@ -34,12 +34,16 @@ constexpr int kGmMaxComp = 8;          // components reduced per sweep over the 
 constexpr int kGmCompLimit = 1920;     // 3 x 8 B x n_comp dynamic + 2 KB static shared memory <= 48 KB
 constexpr int kGmRegComp = 2;        // components kept in registers (others re-read)
 
-template <bool VE>
+// MODE 0: VP eps (denoiser.py:85-107); 1: VE ODE velocity (:124-136);
+// 2: VP posterior mean E[x0 | x_t] (x0_posterior_mean, :110-121).
+template <int MODE>
 __global__ void __launch_bounds__(kGmThreads)
 gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ ts, int64_t D,
               const double* __restrict__ alpha_bar, int T, const double* __restrict__ means,
               const double* __restrict__ log_w, const double* __restrict__ var, int n_comp,
               double* const* __restrict__ outs, int* __restrict__ err) {
+  constexpr bool VE = MODE == 1;
+  constexpr bool X0 = MODE == 2;
   pdl_wait();
   pdl_trigger();
   __shared__ double red[kGmMaxComp][32];
@@ -135,7 +139,8 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
   }
   for (int i = threadIdx.x; i < n_comp; i += blockDim.x) {
     const double sc = VE ? var[i] + one_m : abar * var[i] + one_m;
-    s_sc[i] = VE ? var[i] / sc : sc;       // VE: posterior gain v_i / s_i
+    // VE: posterior gain v_i / s_i; X0: sqrt(abar) v_i / s_i (denoiser.py:117)
+    s_sc[i] = VE ? var[i] / sc : (X0 ? (sa * var[i]) / sc : sc);
   }
   __syncthreads();
 
@@ -161,10 +166,12 @@ gm_eps_kernel(const double* const* __restrict__ xs, const int32_t* __restrict__ 
         for (int i = 0; i < n_comp; ++i) {
           const double m = i < kGmRegComp ? mr[i < kGmRegComp ? i : 0][e] : __ldg(means + (int64_t)i * D + j);
           const double r = s_r[i], sc = s_sc[i];
-          const double term = VE ? r * (m + sc * (xr[e] - m)) : (r * (sa * m - xr[e])) / sc;
+          const double term = VE ? r * (m + sc * (xr[e] - m))
+                            : X0 ? r * (m + sc * (xr[e] - sa * m))          // cond_mean (denoiser.py:118)
+                                 : (r * (sa * m - xr[e])) / sc;
           score = (i == 0) ? term : score + term;
         }
-        out[j] = VE ? (xr[e] - score) / sigma : neg_sq * score;
+        out[j] = VE ? (xr[e] - score) / sigma : (X0 ? score : neg_sq * score);
       }
     }
   }
@@ -180,7 +187,7 @@ extern "C" int drs_gm_eps(const double* const* xs, const int32_t* ts, int n_rows
   if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmCompLimit || T < 0) return DRS_ERR_VALUE;
   if (n_rows == 0 || D == 0) return DRS_OK;
   if (!xs || !ts || !alpha_bar || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
-  drs::launch_pdl(drs::gm_eps_kernel<false>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
+  drs::launch_pdl(drs::gm_eps_kernel<0>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
       xs, ts, D, alpha_bar, T, means, log_w, var, n_comp, out, err);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
@@ -191,7 +198,19 @@ extern "C" int drs_gm_velocity(const double* const* xs, const int32_t* idx, int 
   if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmCompLimit || N < 0) return DRS_ERR_VALUE;
   if (n_rows == 0 || D == 0) return DRS_OK;
   if (!xs || !idx || !sigmas || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
-  drs::launch_pdl(drs::gm_eps_kernel<true>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
+  drs::launch_pdl(drs::gm_eps_kernel<1>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp), (cudaStream_t)stream,
       xs, idx, D, sigmas, N, means, log_w, var, n_comp, out, err);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_gm_x0_mean(const double* const* xs, const int32_t* zeros, int n_rows, int64_t D,
+                              const double* abar, const double* means, const double* log_w, const double* var,
+                              int n_comp, double* const* out, int* err, void* stream) {
+  if (n_rows < 0 || D < 0 || n_comp < 1 || n_comp > drs::kGmCompLimit) return DRS_ERR_VALUE;
+  if (n_rows == 0 || D == 0) return DRS_OK;
+  if (!xs || !zeros || !abar || !means || !log_w || !var || !out || !err) return DRS_ERR_VALUE;
+  // every row reads the same abar: a 1-entry table indexed by t = zeros[r] = 0
+  drs::launch_pdl(drs::gm_eps_kernel<2>, dim3(n_rows), dim3(drs::kGmThreads), drs::gm_smem(n_comp),
+      (cudaStream_t)stream, xs, zeros, D, abar, 0, means, log_w, var, n_comp, out, err);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

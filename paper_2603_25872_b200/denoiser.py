@@ -346,6 +346,34 @@ def velocity_oracle(gm: GaussianMixture, x, sigma: float):
     return out.reshape(xd.shape)
 
 
+def x0_posterior_mean(gm: GaussianMixture, x, abar: float):
+    """E[x_0 | x_t = x] under the same VP noising as eps_oracle (denoiser.py:110-121),
+    on device (K9 posterior-mean mode)."""
+    import torch
+    from .rng import _check_err
+    from .transitions import _device_of, as_device
+    if not 0.0 < abar <= 1.0:
+        raise ValueError(f"abar must lie in (0, 1], got {abar}")
+    dev = _device_of(x)
+    xd = as_device(x, dev, torch.float64)
+    if xd.shape[-1] != gm.dim:
+        raise DimensionMismatch(f"state dim {xd.shape[-1]} != mixture dim {gm.dim}")
+    flat = xd.reshape(-1, gm.dim)
+    out = torch.empty_like(flat)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    means, logw, var = gm.device_params(dev)
+    xs_p = _ptr_array(_rows(flat, gm.dim), dev)
+    out_p = _ptr_array(_rows(out, gm.dim), dev)
+    zeros = torch.zeros(flat.shape[0], dtype=torch.int32, device=dev)
+    table = torch.tensor([float(abar)], dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().drs_gm_x0_mean(xs_p.data_ptr(), zeros.data_ptr(), flat.shape[0], gm.dim,
+                                         table.data_ptr(), means.data_ptr(), logw.data_ptr(), var.data_ptr(),
+                                         len(gm.weights), out_p.data_ptr(), err.data_ptr(), _lib.stream_ptr()),
+               "drs_gm_x0_mean")
+    _check_err(err)
+    return out.reshape(xd.shape)
+
+
 @dataclass(frozen=True, eq=False)
 class EulerVelocity:
     """Engine core of the Euler family: the velocity of `gm` on sigma grid `g`;
@@ -390,9 +418,9 @@ def evaluate(d, s: NoiseSchedule, x, t: int, clock: VirtualClock | None = None):
     if isinstance(d, StateIndependent):
         if t < 0 or t > s.T:
             raise TimestepOutOfRange(f"t={t} outside 0..{s.T}")
-        dev = getattr(x, "device", None)
-        return state_independent_eps(d.seed, t, d.dim,
-                                     device=dev if dev is not None and dev.type == "cuda" else None)
+        import torch
+        dev = x.device if isinstance(x, torch.Tensor) and x.is_cuda else None
+        return state_independent_eps(d.seed, t, d.dim, device=dev)
     if isinstance(d, Perturbed):
         value = evaluate(d.inner, s, x, t, clock)
         if d.scale == 0.0:

@@ -406,7 +406,11 @@ class DeviceRun:
         L = _lib.lib()
         rng_rows, si_rows = self._key_ranges()
         # rng rows come first, si rows after (see _alloc): two contiguous launches
-        if rng_rows:
+        ext = getattr(self, "external_noise", None)
+        if rng_rows and ext is not None:      # caller-supplied rows (an RngStream.derive override)
+            for r, row in zip(rng_rows, ext):
+                self.noise[r].copy_(torch.as_tensor(row).reshape(-1), non_blocking=True)
+        elif rng_rows:
             timed("noise", len(rng_rows) * self.D * 8, lambda: _lib.check(L.drs_noise_fill(
                 GENERATORS[self.generator], self.keybuf.dev.data_ptr(), len(rng_rows), self.seeds.data_ptr(),
                 self.D, self.noise.data_ptr(), self.noise.stride(0), self.err.data_ptr(), stream),

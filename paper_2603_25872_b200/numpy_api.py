@@ -88,6 +88,7 @@ derive_noise = _returns_host(_rng.derive_noise)
 state_independent_eps = _returns_host(_den.state_independent_eps)
 eps_oracle = _returns_host(_den.eps_oracle)
 velocity_oracle = _returns_host(_den.velocity_oracle)
+x0_posterior_mean = _returns_host(_den.x0_posterior_mean)
 evaluate = _returns_host(_den.evaluate)
 
 # ---- transitions (transitions.py:105-188, sequential.py:51-54) ---------------
@@ -100,7 +101,7 @@ predicted_x0 = _returns_host(_seq.predicted_x0)
 @functools.wraps(_tr.ddpm_skip_posterior)
 def ddpm_skip_posterior(*a, **k):
     p = _tr.ddpm_skip_posterior(*a, **k)
-    return SkipPosterior(to_host(p.mean), p.var)
+    return SkipPosterior(to_host(p.mean), p.variance)
 
 
 # ---- samplers / schedulers (sequential.py:57-130, parallel.py:98-381) --------

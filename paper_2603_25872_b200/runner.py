@@ -62,13 +62,16 @@ def get_run(prog_key, build_prog, s, d, D, device, generator, comm: Comm | None)
     return run
 
 
-def execute(run: DeviceRun, x_T, seed: int, clock=None, *, reports: bool = False):
+def execute(run: DeviceRun, x_T, seed: int, clock=None, *, reports: bool = False, noise_rows=None):
     """Run once (eagerly, with per-round CUDA events) and return
-    (Trajectory, [RoundReport]).  x_T: numpy array or tensor of D elements."""
+    (Trajectory, [RoundReport]).  x_T: numpy array or tensor of D elements.
+    noise_rows: the run's rng noise rows supplied by the caller (in program key
+    order) instead of the in-kernel fill."""
     dev = run.device
     x = as_device(x_T, dev, torch.float64)
     shape = tuple(x.shape)
     run.set_inputs(x, seed)
+    run.external_noise = noise_rows
     n_rounds = len(run.prog.rounds)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(n_rounds)]
@@ -78,6 +81,7 @@ def execute(run: DeviceRun, x_T, seed: int, clock=None, *, reports: bool = False
     t1.record()
     traj_buf = run.traj.clone()
     t1.synchronize()
+    run.external_noise = None
     run.check_err()
     per_round = run.account(clock)
     round_ms = [a.elapsed_time(b) for a, b in ev]

@@ -15,6 +15,19 @@ def predicted_x0(s, x_t, eps, t: int):
 
 
 
+def _derived_rows(noise: RngStream, run, x_T):
+    """The reference's sequential samplers draw z through the stream's own
+    method, noise.derive(u, TRANSITION, x.shape) (sequential.py:72,109), so a
+    RngStream subclass may override it.  When it does, the run's noise rows come
+    from that method, called in the reference's order; otherwise the noise
+    kernel generates them in-program (bit-identical to RngStream.derive)."""
+    if type(noise).derive is RngStream.derive:
+        return None
+    from .rng import Role
+    shape = tuple(getattr(x_T, "shape", ())) or (run.D,)
+    return [noise.derive(t, Role(role), shape) for _, t, role in run.prog.noise_keys]
+
+
 def sample_ddpm(s, d, x_T, noise: RngStream, clock=None) -> Trajectory:
     """Ancestral DDPM: T unit-step posterior transitions, z of step t from
     key (t-1, TRANSITION) (sequential.py:57-76)."""
@@ -22,7 +35,7 @@ def sample_ddpm(s, d, x_T, noise: RngStream, clock=None) -> Trajectory:
     rule = VarianceRule.deterministic()
     run = get_run(("seq", "ddpm", s.T), lambda: build_sequential(s, rule, "ddpm"),
                   s, d, _numel(x_T), dev, noise.generator, None)
-    traj, _ = execute(run, x_T, noise.seed, clock)
+    traj, _ = execute(run, x_T, noise.seed, clock, noise_rows=_derived_rows(noise, run, x_T))
     return traj
 
 
@@ -33,7 +46,7 @@ def sample_ddim(s, d, x_T, rule: VarianceRule, noise: RngStream, subsequence=Non
     sub = tuple(subsequence) if subsequence is not None else None
     run = get_run(("seq", "ddim", s.T, rule, sub), lambda: build_sequential(s, rule, "ddim", sub),
                   s, d, _numel(x_T), dev, noise.generator, None)
-    traj, _ = execute(run, x_T, noise.seed, clock)
+    traj, _ = execute(run, x_T, noise.seed, clock, noise_rows=_derived_rows(noise, run, x_T))
     return traj
 
 

@@ -325,3 +325,52 @@ def test_execute_round_perturbed_network_eps(cuda):
     assert e1.dtype == torch.float64 and e1.shape == e0.shape
     want = e0.double() + 0.25 * torch.from_numpy(O.perturbation(_np(x), 7, 1.0)).to(cuda)
     assert torch.allclose(e1, want, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("n_comp", [1, 2, 11])
+def test_x0_posterior_mean_vs_oracle(cuda, n_comp):
+    """x0_posterior_mean (denoiser.py:110-121) on device (K9 posterior-mean mode)."""
+    rng = np.random.default_rng(n_comp + 7)
+    D = 300
+    w = rng.random(n_comp)
+    w /= w.sum()
+    means, var = rng.normal(size=(n_comp, D)), rng.random(n_comp) + 0.3
+    gm = P.GaussianMixture(weights=w, means=means, variances=var)
+    x = rng.normal(size=(4, D))
+    for abar in (1.0, 0.25, 1e-3):
+        got = _np(P.x0_posterior_mean(gm, torch.from_numpy(x).to(cuda), abar))
+        ref = O.gm_x0_mean(w, means, var, x, abar)
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12, (n_comp, abar)
+    with pytest.raises(ValueError):
+        P.x0_posterior_mean(gm, torch.from_numpy(x).to(cuda), 0.0)
+
+
+def test_derive_override_feeds_sequential_samplers(cuda):
+    """A RngStream subclass overriding derive() supplies the sequential
+    samplers' z (sequential.py:72,109 call noise.derive): called once per
+    step in the reference order, and the samples use its values."""
+    calls = []
+
+    class Audit(P.RngStream):
+        def derive(self, t, role, shape, *, device=None):
+            calls.append((t, P.Role(role)))
+            return 2.0 * super().derive(t, role, shape, device=device)     # visibly different noise
+
+    s, D = P.default_schedule(20), 64
+    x = torch.from_numpy(O.derive_noise(1, 20, O.INIT, D)).to(cuda)
+    den = P.StateIndependent(3, D)
+    traj = P.sample_ddim(s, den, x, P.VarianceRule.ddpm_induced(), Audit(seed=1))
+    assert calls == [(u, P.Role.TRANSITION) for u in range(19, -1, -1)]
+    plain = P.sample_ddim(s, den, x, P.VarianceRule.ddpm_induced(), P.RngStream(1))
+    assert not torch.equal(traj.final, plain.final)
+    ab = O.default_alpha_bar(20)
+    xr, ref = _np(x), [(20, _np(x))]
+    for t in range(20, 0, -1):
+        z = 2.0 * O.derive_noise(1, t - 1, O.TRANSITION, D)
+        xr = O.ddim_skip(ab, t, 1, xr, O.SI(3, D)(ab, xr, t), ("ddpm",), z)
+        ref.append((t - 1, xr))
+    for (_, g), (_, r) in zip(traj.states, ref):
+        assert np.array_equal(_np(g), r)
+    calls.clear()
+    P.sample_ddpm(s, den, x, Audit(seed=1))
+    assert calls == [(t - 1, P.Role.TRANSITION) for t in range(20, 0, -1)]

@@ -169,6 +169,9 @@ int drs_version(void);
 /* 1: launch every kernel with programmatic dependent launch so its prologue
  * overlaps the predecessor's tail; 0 (default): plain stream ordering. */
 int drs_set_pdl(int on);
+/* 1 (default): GEMM producers request their first weight (B) tiles before the
+ * PDL wait, overlapping the cold weight stream with the predecessor kernel. */
+int drs_set_early_weights(int on);
 
 #ifdef __cplusplus
 }

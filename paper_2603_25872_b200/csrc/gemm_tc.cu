@@ -144,6 +144,7 @@ struct EpiParams {
   int tma_res;              // 1: residual tile TMA-loaded into the staging buffer (OutMaps::r)
   void* out2;               // kEpi 4: a bf16 copy of the (fp32) output, row stride ldo2
   int64_t ldo2;
+  int early_b;              // 1: weight tiles of the first stages requested before the PDL wait
 };
 
 // kEpi 4: the finished row segment (32 values) also goes to the bf16 copy
@@ -563,13 +564,32 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  pdl_wait();       // everything above is data-independent setup (PDL overlap)
+  // everything above is data-independent setup (PDL overlap); the producer
+  // warp additionally issues its first weight tiles before its wait (below)
+  if (warp != 0) pdl_wait();
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (tc::elect_one()) {
+      // The B operand (weights) is never written by a predecessor kernel: the
+      // B tiles of the first kStages k-blocks are requested BEFORE the PDL wait,
+      // so the cold weight stream overlaps the previous kernel's tail (the
+      // stage's full barrier also expects the A bytes, which follow the wait).
+      int pre = 0;
+      if ((int)blockIdx.x < num_tiles) {
+        const int sp = blockIdx.x % split, mn = blockIdx.x / split;
+        const int mt = mn % m_tiles, nt = mn / m_tiles;
+        const int kb0 = sp * kb_per_split, kb1 = min(num_kb_total, kb0 + kb_per_split);
+        pre = ep.early_b ? max(0, min(kStages, kb1 - kb0)) : 0;
+        for (int j = 0; j < pre; ++j) {
+          uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
+          tc::mbar_arrive_expect_tx(&full_bar[j], S::kStageBytes);
+          tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+        }
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -579,10 +599,11 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
         const int kb0 = sp * kb_per_split;
         const int kb1 = min(num_kb_total, kb0 + kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          const bool b_done = tile == (int)blockIdx.x && kb - kb0 < pre;   // weights already in flight
+          if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
           if (cv.on) {
             const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
             const int ky = tap / 3, kx = tap - ky * 3;
@@ -592,7 +613,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
           } else {
             tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
           }
-          tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+          if (!b_done)
+            tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -863,23 +885,38 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
   __syncthreads();
   pair_sync();                                      // barriers and TMEM of both CTAs are ready
   tc::tc_fence_after();
-  pdl_wait();
+  if (warp != 0) pdl_wait();                       // producer: after its early weight loads (below)
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs: own A rows, half of B) ----------------
     if (tc::elect_one()) {
+      // weight (B) halves of the first kStages k-blocks before the PDL wait (as in
+      // gemm_bf16_tc_kernel): they never depend on a predecessor kernel
+      int pre = 0;
+      if (t0 < num_tiles) {
+        const int pmt = t0 % pm_tiles, nt = t0 / pm_tiles;
+        pre = ep.early_b ? min(kStages, num_kb) : 0;
+        for (int j = 0; j < pre; ++j) {
+          uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * S::kStageBytes);
+          tma_load_2d_pair(&tmap_b, &full_bar[j], sb, j * kBK,
+                           nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+        }
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = t0; tile < num_tiles; tile += tstep) {
         const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
         const int m0 = (pmt * 2 + rank) * kBM;
         for (int kb = 0; kb < num_kb; ++kb) {
-          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          const bool b_done = tile == t0 && kb < pre;
+          if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          if (rank == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
           if (cv.on) {
             const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
             const int ky = tap / 3, kx = tap - ky * 3;
@@ -889,8 +926,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
           } else {
             tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
           }
-          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
-                           nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+          if (!b_done)
+            tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
+                             nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -1056,19 +1094,29 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   __syncthreads();
   pair_sync();                                      // barriers and TMEM of the whole cluster are ready
   tc::tc_fence_after();
-  pdl_wait();
+  if (warp != 0) pdl_wait();                       // producer: after its early weight loads (below)
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (tc::elect_one()) {
+      // weight (B) halves of the first kStages k-blocks before the PDL wait
+      const int pre = ep.early_b ? max(0, min(kStages, kb1 - kb0)) : 0;
+      for (int j = 0; j < pre; ++j) {
+        uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
+        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * S::kStageBytes);
+        tma_load_2d_pair(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK,
+                         nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+        const bool b_done = kb - kb0 < pre;
+        if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * S::kStageBytes;
         uint8_t* sb = sa + S::kABytes;
-        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+        if (half == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
         if (cv.on) {
           const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
           const int ky = tap / 3, kx = tap - ky * 3;
@@ -1078,8 +1126,9 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         } else {
           tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
         }
-        tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
-                         nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+        if (!b_done)
+          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
+                           nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
@@ -1528,7 +1577,8 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
     cv.b_img_off = g->b_img_off;
   }
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
-               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0, g->out2, g->ldo2};
+               g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0, g->out2, g->ldo2,
+               early_weights_enabled()};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   OutMaps tcm;
   memset(&tcm, 0, sizeof(tcm));

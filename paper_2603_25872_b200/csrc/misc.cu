@@ -73,3 +73,8 @@ extern "C" int drs_set_pdl(int on) {
   drs::pdl_enabled() = on ? 1 : 0;
   return DRS_OK;
 }
+
+extern "C" int drs_set_early_weights(int on) {
+  drs::early_weights_enabled() = on ? 1 : 0;
+  return DRS_OK;
+}

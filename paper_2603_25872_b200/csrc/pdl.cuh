@@ -21,6 +21,13 @@ inline int& pdl_enabled() {
   return on;
 }
 
+// runtime switch (drs_set_early_weights): GEMM producers request their first
+// weight tiles before griddepcontrol.wait (weights are never produced on-stream)
+inline int& early_weights_enabled() {
+  static int on = 1;
+  return on;
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -27,6 +27,33 @@ from .transitions import ops_to_device
 _OP_BYTES = _lib.ctypes.sizeof(_lib.DrsOp)
 
 
+class _nvtx:
+    """NVTX range around a libdrs launch group (ncu --nvtx / nsys timelines: noise,
+    eval_<kind>, chain, gather, spin), a no-op without CUDA."""
+
+    def __init__(self, label):
+        self.label = label
+
+    def __enter__(self):
+        if torch.cuda.is_available():
+            torch.cuda.nvtx.range_push(self.label)
+
+    def __exit__(self, *a):
+        if torch.cuda.is_available():
+            torch.cuda.nvtx.range_pop()
+
+
+def _nvtx_mark(msg):
+    """NVTX marker at the start of every scheduler round (round index, anchor t, tasks)."""
+    if torch.cuda.is_available():
+        torch.cuda.nvtx.mark(msg)
+
+
+def _n_tasks(low):
+    """Evaluations in a lowered eval payload (a Perturbed payload wraps the core one)."""
+    return _n_tasks(low[1]) if low[0] == "pert" else low[1]["n_tasks"]
+
+
 def unwrap(d):
     """(core denoiser, eval latency ms (sum of nested Latency), [Counting wrappers])."""
     lat, counters = 0.0, []
@@ -211,7 +238,7 @@ class DeviceRun:
                 self.launches.append(("gather", st.round))
             elif isinstance(st, Noise):
                 pass
-        self.local_evals = sum(payload[1][1]["n_tasks"] for kind, payload in self.launches
+        self.local_evals = sum(_n_tasks(payload[1]) for kind, payload in self.launches
                                if kind == "eval" and payload[1] is not None)
         self.n_ops = len(ops_all)
         self.ops_dev = ops_to_device(ops_all, self.device) if ops_all else None
@@ -334,10 +361,12 @@ class DeviceRun:
     def _timed(self, timers):
         def timed(label, nbytes, fn):
             if timers is None:
-                return fn()
+                with _nvtx(label):
+                    return fn()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            fn()
+            with _nvtx(label):
+                fn()
             e1.record()
             timers.append((label, nbytes, e0, e1))
         return timed
@@ -366,10 +395,12 @@ class DeviceRun:
                 rnd, lowered = payload
                 if events is not None:
                     events[rnd][0].record()
+                info = self.prog.rounds[rnd]
+                _nvtx_mark(f"round {rnd}: anchor t={info.anchor_t}, {info.n_tasks} eval(s)")
                 if lowered is not None:
                     if self.eval_ms > 0:
                         timed("spin", 0, lambda: _lib.check(
-                            L.drs_spin(self.eval_ms * 1000.0, lowered[1]["n_tasks"], stream), "drs_spin"))
+                            L.drs_spin(self.eval_ms * 1000.0, _n_tasks(lowered), stream), "drs_spin"))
                     timed("eval_" + lowered[0], nbytes, lambda: self._launch_eval(lowered, stream))
                 if events is not None and not self._gathered(rnd):
                     events[rnd][1].record()

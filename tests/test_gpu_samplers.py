@@ -374,3 +374,45 @@ def test_derive_override_feeds_sequential_samplers(cuda):
     calls.clear()
     P.sample_ddpm(s, den, x, Audit(seed=1))
     assert calls == [(t - 1, P.Role.TRANSITION) for t in range(20, 0, -1)]
+
+
+def test_realtime_speedup_laws_spin_latency(cuda):
+    """Real-time latency-law calibration (reference tests/test_acceptance.py:164-203,
+    SURVEY 8(d)): the Latency denoiser occupies the GPU for eval_time_ms per round
+    (drs_spin, all tasks of a round concurrently), T = 48; measured wall-clock
+    speedup of both schedulers >= 0.9x the round law T/rounds for devices 2..4,
+    and aggressive devices = 3 >= 2.5x.  Host wall clock around the public call,
+    min over 2 repeats, as the reference."""
+    import time
+    T, eval_ms = 48, 20.0
+    s = P.default_schedule(T)
+    den = P.Latency(P.AnalyticEps(P.standard_normal_mixture(1)),
+                    P.LatencyModel(eval_time_ms=eval_ms, dispatch_overhead_ms=0.2))
+    rule, stream = P.VarianceRule.deterministic(), P.RngStream(seed=0)
+    x_T = P.derive_noise(stream, T, P.Role.INIT, 1, device=cuda)
+
+    def timed(fn, repeats=2):
+        best = math.inf
+        for _ in range(repeats):
+            torch.cuda.synchronize()
+            t0 = time.monotonic()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, (time.monotonic() - t0) * 1000.0)
+        return best
+
+    timed(lambda: P.run_aggressive(s, den, x_T, 2, rule, stream), 1)           # build + warm the programs
+    seq_ms = timed(lambda: P.sample_ddim(s, den, x_T, rule, stream))
+    assert seq_ms >= T * eval_ms
+    fails = []
+    for devices in (2, 3, 4):
+        for runner, rounds in ((P.run_aggressive, 1 + math.ceil(T / devices)),
+                               (P.run_conservative, 2 * math.ceil(T / (devices + 1)))):
+            timed(lambda: runner(s, den, x_T, devices, rule, stream), 1)
+            par_ms = timed(lambda: runner(s, den, x_T, devices, rule, stream))
+            speedup, theory = seq_ms / par_ms, T / rounds
+            if speedup < 0.9 * theory:
+                fails.append((runner.__name__, devices, speedup, theory))
+            if runner is P.run_aggressive and devices == 3:
+                assert speedup >= 2.5, speedup
+    assert not fails, fails

@@ -17,10 +17,12 @@ def main():
     ap.add_argument("--batches", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--early", type=int, default=1, help="GEMM weight tiles requested before the PDL wait")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import _lib
     _lib.lib().drs_set_pdl(a.pdl)
+    _lib.lib().drs_set_early_weights(a.early)
     dev = torch.device("cuda", 0)
     if a.net == "dit":
         from paper_2603_25872_b200.dit import DiT, DiTConfig

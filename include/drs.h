@@ -101,6 +101,8 @@ typedef struct drs_op {
  * sequential.py:68-74,106-111: a draft fan-out, a refine chain, or a refine
  * chain fused with the next block's drafts, in one launch. n_ops <= 64. */
 int drs_skip_chain(const drs_op* ops, int n_ops, int64_t D, void* stream);
+/* Measurement switch: 1 (default) = 16-byte vector kernel for HBM-sized even D, 0 = scalar kernel. */
+int drs_set_chain_vec(int on);
 
 /* ---- toy eps oracle (K9) ------------------------------------------------- */
 #define DRS_GM_MAX_COMP 1920   /* mixture components per launch (shared-memory bound) */

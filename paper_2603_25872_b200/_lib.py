@@ -120,6 +120,7 @@ _SIGS = {
     "drs_version": (ctypes.c_int, []),
     "drs_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_early_weights": (ctypes.c_int, [ctypes.c_int]),
+    "drs_set_chain_vec": (ctypes.c_int, [ctypes.c_int]),
     # include/drs_net.h
     "drs_gemm_bf16": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,

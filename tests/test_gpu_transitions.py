@@ -56,14 +56,29 @@ def test_random_skips_bit_exact(cuda, T):
         assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (t, k)
 
 
-def test_fused_chain_matches_unfused(cuda):
-    """One drs_skip_chain launch over a refine chain + fan-out == op-by-op numpy."""
+@pytest.mark.parametrize("D,vec,offset", [(16384, 1, 0), (1 << 19, 1, 0), (1 << 19, 0, 0), (1 << 19, 1, 1),
+                                          ((1 << 19) + 6, 1, 0)])
+def test_fused_chain_matches_unfused(cuda, D, vec, offset):
+    """One drs_skip_chain launch over a refine chain + fan-out == op-by-op numpy,
+    bit for bit: the latency-bound path (16 K), and for HBM-sized latents the
+    16-byte vector kernel (vec = 1), the scalar kernel (vec = 0) and the vector
+    kernel on rows at an odd element offset (8-byte aligned only: scalar access
+    for those ops)."""
+    from paper_2603_25872_b200 import _lib, default_schedule, VarianceRule
+    from paper_2603_25872_b200.transitions import ddim_op_coeffs, ddpm_op_coeffs, launch_chain, make_op, ops_to_device
+    _lib.lib().drs_set_chain_vec(vec)
+    try:
+        _fused_chain_case(cuda, D, offset)
+    finally:
+        _lib.lib().drs_set_chain_vec(1)
+
+
+def _fused_chain_case(cuda, D, offset):
     from paper_2603_25872_b200 import _lib, default_schedule, VarianceRule
     from paper_2603_25872_b200.transitions import ddim_op_coeffs, ddpm_op_coeffs, launch_chain, make_op, ops_to_device
     s = default_schedule(50)
     ab = O.default_alpha_bar(50)
     rng = np.random.default_rng(0)
-    D = 16384
     x = rng.normal(size=D)
     eps = rng.normal(size=(6, D))
     z = rng.normal(size=(6, D))
@@ -71,7 +86,15 @@ def test_fused_chain_matches_unfused(cuda):
     ed = torch.from_numpy(eps).to(cuda)
     ed32 = ed.float()
     zd = torch.from_numpy(z).to(cuda)
-    outs = torch.zeros(8, D, dtype=torch.float64, device=cuda)
+    if offset:                   # same values in views starting one element in (8-byte aligned)
+        def shifted(t):
+            buf = torch.zeros(t.numel() + offset * t.shape[0] + 8, dtype=t.dtype, device=cuda)
+            v = buf[offset:offset + t.numel()].view(t.shape)
+            v.copy_(t)
+            return v
+        xd, ed, zd = shifted(xd), shifted(ed), shifted(zd)
+        ed32 = shifted(ed32)
+    outs = torch.zeros(8 * D + 1, dtype=torch.float64, device=cuda)[offset:offset + 8 * D].view(8, D)
     rule = VarianceRule.ddpm_induced()
     ops = []
     for i in range(4):   # refine chain 40 -> 36

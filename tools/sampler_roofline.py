@@ -40,6 +40,8 @@ def timeit(fn, reps=30):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--log2d", type=int, default=25)
+    ap.add_argument("--vec", type=int, default=1,
+                    help="skip-chain kernel for HBM-sized latents: 0 scalar, 1 16-byte vector (1 pair/thread), 2 (2 pairs)")
     a = ap.parse_args()
     import torch
 
@@ -55,6 +57,7 @@ def main():
     except Exception:
         peak, src = 7700.0, "B200_PROFILING.md fallback"
     dev = torch.device("cuda", 0)
+    _lib.lib().drs_set_chain_vec(a.vec)
     D = 1 << a.log2d
     s = P.default_schedule(50)
     x = torch.randn(D, dtype=torch.float64, device=dev)
@@ -106,6 +109,7 @@ def main():
         t = timeit(lambda: fill_streams(kb, n, tab, gen, err=err), 10)
         gbs = 8 * ns * n / t / 1e9
         rows.append((f"noise {gen} ({ns} streams x {n} draws)", 8, t * 1e6, gbs, gbs / peak))
+    print(f"# chain kernel: {['scalar (skip_chain_kernel)', '16-byte vector, 1 pair/thread', '16-byte vector, 2 pairs/thread'][a.vec]}")
     print(f"# D = 2^{a.log2d} = {D} elements (fp64 state: {8 * D / 2**20:.0f} MiB per array, > 126 MB L2); "
           f"peak {peak} GB/s ({src})")
     for label, bpe, us, gbs, frac in rows:

@@ -109,6 +109,12 @@ int drs_attention_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, con
                      int vt_img, void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale,
                      void* stream);
 
+/* Same with V row-major -- v[b*Lk + key, h*d + j] (row stride ldv), e.g. the V block
+ * of one fused QKV projection -- loaded like K and read by the PV MMA as an
+ * MN-major B operand (no V^T GEMM).  d % 8 == 0, d <= 192. */
+int drs_attention_tc_v(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                       void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale, void* stream);
+
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);
 int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out_bf16, void* stream);

@@ -157,7 +157,10 @@ __device__ __forceinline__ int sw128_off(int row, int c) {
   return (c >> 3) * (kAQ * 128) + (row >> 3) * 1024 + (row & 7) * 128 + (((c & 7) ^ (row & 7)) << 4);
 }
 
-template <int DP, int NPOLY>
+// VROW: V given row-major (keys x channels, the V block of a fused QKV GEMM
+// output) and loaded exactly like K; the PV MMA reads it as an MN-major B
+// operand (b_major = 1) -- no separate V^T GEMM.  Otherwise V^T (channels x keys).
+template <int DP, int NPOLY, bool VROW>
 __global__ void __launch_bounds__(kAttnTcThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
@@ -183,7 +186,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int q0 = blockIdx.x * kAQ, h = blockIdx.y, b = blockIdx.z;
   const int n_tiles = (Lk + kAK - 1) / kAK;
   constexpr uint32_t kIdescS = tc::idesc_bf16_f32(128, kAK);
-  constexpr uint32_t kIdescO = tc::idesc_bf16_f32(128, DP);
+  constexpr uint32_t kIdescO = VROW ? tc::idesc_bf16_f32_bmn(128, DP) : tc::idesc_bf16_f32(128, DP);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tm_q);
@@ -237,8 +240,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         tc::mbar_wait(&v_empty[st], ((j / kSt) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&v_full[st], S::kVBytes);
         uint8_t* v_dst = sV + st * S::kVBytes;
-        for (int a = 0; a < kAK / 64; ++a)
-          tc::tma_load_2d(&tm_vt, &v_full[st], v_dst + a * (DP * 128), b * vt_img + j * kAK + a * 64, h * d);
+        if constexpr (VROW) {              // [128 keys x 64 ch] atoms, like the K tile
+          for (int a = 0; a < S::kAtoms; ++a)
+            tma_load_3d(&tm_vt, &v_full[st], v_dst + a * (kAK * 128), a * 64, h, b * Lk + j * kAK);
+        } else {
+          for (int a = 0; a < kAK / 64; ++a)
+            tc::tma_load_2d(&tm_vt, &v_full[st], v_dst + a * (DP * 128), b * vt_img + j * kAK + a * 64, h * d);
+        }
       }
     }
   } else if (warp == 1) {
@@ -279,9 +287,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const uint8_t* vb = sV + st * S::kVBytes;
         const uint32_t o_col = 256 + (kSets == 2 ? (j & 1) * DP : 0);
 #pragma unroll
-        for (int kk = 0; kk < kAK / 16; ++kk)
-          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), kdesc(vb, kk, DP * 128),
+        for (int kk = 0; kk < kAK / 16; ++kk) {
+          // VROW: 16 keys = 16 rows of 128 B per K step; channel atoms kAK * 128 B apart
+          const uint64_t bdesc = VROW ? tc::smem_desc_sw128_mn(vb + kk * 2048, kAK * 128) : kdesc(vb, kk, DP * 128);
+          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), bdesc,
                        kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
+        }
         tc::mma_commit(&v_empty[st]);
         tc::mma_commit(&o_done[j & 1]);
       }
@@ -533,11 +544,11 @@ static bool tmap_vt(CUtensorMap* m, const void* ptr, int64_t chans, int64_t keys
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DP, int NPOLY>
+template <int DP, int NPOLY, bool VROW>
 static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                          int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   using S = AttnSmem<DP>;
-  auto kern = attn_tc_kernel<DP, NPOLY>;
+  auto kern = attn_tc_kernel<DP, NPOLY, VROW>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
@@ -549,13 +560,13 @@ static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
-template <int DP>
+template <int DP, bool VROW>
 static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                        int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   static int npoly = [] { const char* e = getenv("DRS_ATTN_POLY"); return e ? atoi(e) : 2; }();
-  if (npoly == 0) return launch_attn_v<DP, 0>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  if (npoly == 3) return launch_attn_v<DP, 3>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  return launch_attn_v<DP, 2>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (npoly == 0) return launch_attn_v<DP, 0, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (npoly == 3) return launch_attn_v<DP, 3, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  return launch_attn_v<DP, 2, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
 }
 
 }  // namespace drs
@@ -577,9 +588,30 @@ extern "C" int drs_attention_tc(const void* q, int64_t ldq, const void* k, int64
     return DRS_ERR_CUDA;
   const float sl2 = scale * 1.4426950408889634f;
   cudaStream_t st = (cudaStream_t)stream;
-  if (DP == 64) return launch_attn<64>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  if (DP == 128) return launch_attn<128>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  return launch_attn<192>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (DP == 64) return launch_attn<64, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (DP == 128) return launch_attn<128, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  return launch_attn<192, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+}
+
+// V row-major (the V block of a fused QKV projection), read as an MN-major PV operand
+extern "C" int drs_attention_tc_v(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                  int64_t ldv, void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d,
+                                  float scale, void* stream) {
+  using namespace drs;
+  if (B <= 0 || H <= 0 || Lq <= 0 || Lk <= 0 || d <= 0 || d > 192 || d % 8) return DRS_ERR_VALUE;
+  if ((ldq | ldk | ldv | ldo) % 8 || (reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+                                      reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
+    return DRS_ERR_VALUE;
+  const int DP = d <= 64 ? 64 : (d <= 128 ? 128 : 192);
+  CUtensorMap tq, tk, tv, to;
+  if (!tmap_heads(&tq, q, (int64_t)B * Lq, H, d, ldq) || !tmap_heads(&tk, k, (int64_t)B * Lk, H, d, ldk) ||
+      !tmap_heads(&tv, v, (int64_t)B * Lk, H, d, ldv) || !tmap_out(&to, o, B, Lq, H, d, ldo))
+    return DRS_ERR_CUDA;
+  const float sl2 = scale * 1.4426950408889634f;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (DP == 64) return launch_attn<64, true>(tq, tk, tv, to, B, H, Lq, Lk, d, Lk, sl2, st);
+  if (DP == 128) return launch_attn<128, true>(tq, tk, tv, to, B, H, Lq, Lk, d, Lk, sl2, st);
+  return launch_attn<192, true>(tq, tk, tv, to, B, H, Lq, Lk, d, Lk, sl2, st);
 }
 
 extern "C" int drs_attention_tc_debug(int* mapped_trace) {

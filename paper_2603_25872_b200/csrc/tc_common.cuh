@@ -105,9 +105,27 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* tile) {
   d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
   return d;
 }
+// MN-major operand tile staged by TMA with SWIZZLE_128B: rows of 64 bf16 MN
+// elements (128 B) along K, 8-row K groups 1024 B apart (SBO), 64-element MN
+// atoms `lbo_bytes` apart (LBO) -- the canonical ((8,n),(8,k)):((1,LBO),(8,SBO))
+// layout of cute's make_umma_desc<Major::MN> in 16-byte units.
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(const void* tile, uint32_t lbo_bytes) {
+  const uint64_t addr = smem_u32(tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;                // start address
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;   // LBO: next 64-element MN atom
+  d |= (uint64_t)(1024 >> 4) << 32;            // SBO: next 8 K-rows
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
 // kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both K-major
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+// ... with B MN-major (bit 16: b_major)
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(uint32_t M, uint32_t N) {
+  return idesc_bf16_f32(M, N) | (1u << 16);
 }
 
 __device__ __forceinline__ bool elect_one() {

@@ -19,6 +19,7 @@ The 28 x 4 GEMMs run on the tcgen05 kernel (drs_gemm); the adaLN
 gate multiply and the residual add are fused into their epilogues.
 """
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -117,8 +118,11 @@ class DiT:
         self.pos_b = self.w.pos.repeat(max_batch, 1).contiguous()        # (MB, h) fp32 residual for x-embed
         self.hs = torch.empty(MB, h, dtype=f32, device=dev)               # residual stream
         self.xn = torch.empty(MB, h, dtype=bf, device=dev)
-        self.qkv = torch.empty(MB, 2 * h, dtype=bf, device=dev)            # Q | K
-        self.vt = torch.empty(h, MB, dtype=bf, device=dev)                 # V^T (swapped GEMM)
+        # one fused QKV GEMM; the attention reads V row-major as an MN-major operand
+        # (DRS_QKV_FUSED=0: Q|K GEMM + swapped V^T GEMM, the round-1 layout)
+        self.fused_qkv = os.environ.get("DRS_QKV_FUSED", "1") != "0"
+        self.qkv = torch.empty(MB, 3 * h, dtype=bf, device=dev)            # Q | K | V
+        self.vt = torch.empty(h, MB, dtype=bf, device=dev)                 # V^T (unfused layout only)
         self.att = torch.empty(MB, h, dtype=bf, device=dev)
         self.mlp = torch.empty(MB, m, dtype=bf, device=dev)
         self.tout = torch.empty(MB, cfg.patch * cfg.patch * cfg.out_ch, dtype=f32, device=dev)
@@ -158,13 +162,20 @@ class DiT:
             sh_m, sc_m, g_m = (md[:, base + 3 * h:base + 4 * h], md[:, base + 4 * h:base + 5 * h],
                                md[:, base + 5 * h:base + 6 * h])
             ops.layernorm(hs, out=xn, shift=sh_a, scale=sc_a, eps=1e-6, mod_group=T)
-            ops.linear(xn, blk["qkv_w"][:2 * h], bias=blk["qkv_b"][:2 * h], out=qkv)
-            # V^T = W_v xn^T: the tcgen05 attention consumes V transposed.  The V bias is
-            # folded into the projection bias (softmax rows sum to 1: P (V + 1 b_v^T) = P V + b_v)
-            ops.linear(blk["qkv_w"][2 * h:], xn, out=self.vt[:, :M])
-            ops.attention_tc(qkv[:, 0:h], qkv[:, h:2 * h], self.vt[:, :M], att, B, cfg.heads, T, T,
-                             h // cfg.heads, vt_img=T)
-            ops.linear(att, blk["proj_w"], bias=blk["proj_b_eff"], colscale=g_a, cs_group=T, residual=hs, out=hs)
+            if self.fused_qkv:
+                ops.linear(xn, blk["qkv_w"], bias=blk["qkv_b"], out=qkv)
+                ops.attention_qkv(qkv[:, 0:h], qkv[:, h:2 * h], qkv[:, 2 * h:3 * h], att, B, cfg.heads, T, T,
+                                  h // cfg.heads)
+                proj_b = blk["proj_b"]
+            else:
+                ops.linear(xn, blk["qkv_w"][:2 * h], bias=blk["qkv_b"][:2 * h], out=qkv[:, :2 * h])
+                # V^T = W_v xn^T for the V^T attention path.  The V bias is folded into the
+                # projection bias (softmax rows sum to 1: P (V + 1 b_v^T) = P V + b_v)
+                ops.linear(blk["qkv_w"][2 * h:], xn, out=self.vt[:, :M])
+                ops.attention_tc(qkv[:, 0:h], qkv[:, h:2 * h], self.vt[:, :M], att, B, cfg.heads, T, T,
+                                 h // cfg.heads, vt_img=T)
+                proj_b = blk["proj_b_eff"]
+            ops.linear(att, blk["proj_w"], bias=proj_b, colscale=g_a, cs_group=T, residual=hs, out=hs)
             ops.layernorm(hs, out=xn, shift=sh_m, scale=sc_m, eps=1e-6, mod_group=T)
             ops.linear(xn, blk["fc1_w"], bias=blk["fc1_b"], act="gelu_tanh", out=mlp)
             ops.linear(mlp, blk["fc2_w"], bias=blk["fc2_b"], colscale=g_m, cs_group=T, residual=hs, out=hs)

@@ -188,6 +188,17 @@ def attention_tc(q, k, vt, out, B, H, Lq, Lk, d, scale=None, vt_img=None):
     return out
 
 
+def attention_qkv(q, k, v, out, B, H, Lq, Lk, d, scale=None):
+    """tcgen05 attention with V row-major (B*Lk rows, head h at column h*d):
+    the Q / K / V column blocks of one fused QKV GEMM output, no V^T GEMM."""
+    scale = d ** -0.5 if scale is None else scale
+    st = _lib.lib().drs_attention_tc_v(q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(),
+                                       v.stride(0), out.data_ptr(), out.stride(0), B, H, Lq, Lk, d, float(scale),
+                                       _lib.stream_ptr())
+    _lib.check(st, "drs_attention_tc_v")
+    return out
+
+
 def timestep_embedding(t, dim, out, max_period=10000.0):
     _lib.check(_lib.lib().drs_timestep_embedding(t.data_ptr(), t.numel(), dim, float(max_period), out.data_ptr(),
                                                  _lib.stream_ptr()), "drs_timestep_embedding")

@@ -82,6 +82,9 @@ class UNet:
         self.ctx_pad = (cfg.ctx_len + 7) // 8 * 8
         # cross-attention folded into two GEMMs against the fixed context (DRS_FOLD_CROSS=0: attention kernel)
         self.fold_cross = os.environ.get("DRS_FOLD_CROSS", "1") != "0"
+        # self-attention Q, K, V from ONE GEMM; the attention kernel reads V row-major
+        # (DRS_QKV_FUSED=0: Q|K GEMM + swapped V^T GEMM, the round-1 layout)
+        self.fused_qkv = os.environ.get("DRS_QKV_FUSED", "1") != "0"
         I = _Init(self.device, seed)
         c0, T = cfg.channels[0], cfg.temb_dim
         self.p = p = {}
@@ -278,16 +281,22 @@ class UNet:
         s = self.buf(f"txs{c}_{HW}", (M, c), torch.float32)                   # fp32 residual stream
         self._lin(hn, t["pin"][0], bias=t["pin"][1], out=s)
         n1 = self.buf(f"txn{c}_{HW}", (M, c))
-        qk = self.buf(f"qk{c}_{HW}", (M, 2 * c))
-        vt = self.buf(f"vt{c}_{HW}", (c, M))
+        qk = self.buf(f"qkv{c}_{HW}", (M, 3 * c))           # Q | K | V (V^T in vt if not fused)
+        vt = None if self.fused_qkv else self.buf(f"vt{c}_{HW}", (c, M))
         att = self.buf(f"att{c}_{HW}", (M, c))
         ffb = self.buf(f"ff{c}_{HW}", (M, 4 * c))
         sb = self.buf(f"txsb{c}_{HW}", (M, c))              # bf16 copy of the stream for proj_out
         for L in t["layers"]:
             ops.layernorm(s, out=n1, gamma=L["ln1"][0], beta=L["ln1"][1], eps=1e-5)
-            self._lin(n1, L["qkv"][:2 * c], out=qk)                       # Q | K
-            self._lin(L["qkv"][2 * c:], n1, out=vt)                       # V^T = Wv n1^T (swapped GEMM)
-            self._attn(qk[:, :c], qk[:, c:], vt, att, N, heads, HW, HW, d, HW)
+            if self.fused_qkv:      # one QKV GEMM; attention reads V row-major (MN-major PV operand)
+                self._lin(n1, L["qkv"], out=qk)
+                if self._count:
+                    self.flops += 4.0 * N * heads * HW * HW * d
+                ops.attention_qkv(qk[:, :c], qk[:, c:2 * c], qk[:, 2 * c:], att, N, heads, HW, HW, d)
+            else:
+                self._lin(n1, L["qkv"][:2 * c], out=qk[:, :2 * c])           # Q | K
+                self._lin(L["qkv"][2 * c:], n1, out=vt)                       # V^T = Wv n1^T (swapped GEMM)
+                self._attn(qk[:, :c], qk[:, c:2 * c], vt, att, N, heads, HW, HW, d, HW)
             self._lin(att, L["o1"][0], bias=L["o1"][1], residual=s, out=s)
             ops.layernorm(s, out=n1, gamma=L["ln2"][0], beta=L["ln2"][1], eps=1e-5)
             if "ws" in L and HW % 128 == 0 and self.fold_cross:

@@ -267,3 +267,34 @@ def test_sd15_cross_attention_fold_batched(cuda, size, B, g):
         for b in range(B):
             rel = ((o[b].reshape(4, size, size) - ref[b]).norm() / ref[b].norm()).item()
             assert rel < 3e-2, (fold, b, rel)
+
+
+@pytest.mark.parametrize("B,H,Lq,Lk,d,amp", [(2, 8, 1024, 1024, 40, 1), (1, 16, 256, 256, 72, 1),
+                                             (2, 10, 256, 256, 64, 1), (1, 5, 300, 333, 64, 6),
+                                             (3, 4, 70, 300, 160, 1), (2, 2, 129, 77, 96, 6),
+                                             (2, 20, 64, 64, 64, 1), (2, 8, 4096, 4096, 40, 1)])
+def test_attention_qkv_rowmajor_v(cuda, B, H, Lq, Lk, d, amp):
+    """tcgen05 attention reading V row-major from a fused QKV buffer (MN-major PV
+    operand) vs torch fp32, and equal to the V^T path up to fp32 summation order."""
+    from paper_2603_25872_b200.netops import attention_qkv, attention_tc
+    g = torch.Generator(device=cuda).manual_seed(Lq * 3 + d)
+    qkv_q = (amp * torch.randn(B * Lq, 3 * H * d, device=cuda, generator=g)).bfloat16()
+    kv = torch.randn(B * Lk, 3 * H * d, device=cuda, generator=g).bfloat16()
+    q, k, v = qkv_q[:, :H * d], kv[:, H * d:2 * H * d], kv[:, 2 * H * d:]
+    full = torch.full((B * Lq + 130, H * d), 7.0, device=cuda, dtype=torch.bfloat16)
+    out = full[:B * Lq]
+    attention_qkv(q, k, v, out, B, H, Lq, Lk, d)
+    Q = q.float().reshape(B, Lq, H, d).transpose(1, 2)
+    K = k.float().reshape(B, Lk, H, d).transpose(1, 2)
+    V = v.float().reshape(B, Lk, H, d).transpose(1, 2)
+    ref = (torch.softmax(Q @ K.transpose(-1, -2) / math.sqrt(d), -1) @ V).transpose(1, 2).reshape(B * Lq, H * d)
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
+    assert bool((full[B * Lq:] == 7.0).all())
+    vimg = (Lk + 7) // 8 * 8
+    vt = torch.zeros(H * d, B * vimg, device=cuda, dtype=torch.bfloat16)
+    for b in range(B):
+        vt[:, b * vimg:b * vimg + Lk] = v[b * Lk:(b + 1) * Lk].t()
+    out_t = torch.empty_like(out)
+    attention_tc(q, k, vt, out_t, B, H, Lq, Lk, d, vt_img=vimg)
+    assert ((out.float() - out_t.float()).abs().max() <= 1e-2 * ref.abs().max()).item()

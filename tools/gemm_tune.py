@@ -121,6 +121,7 @@ def main():
     ap.add_argument("--cold", action="store_true", help="weights streamed from HBM (rotating copies)")
     ap.add_argument("--mmax", type=int, default=0, help="only shapes with M <= mmax")
     ap.add_argument("--merge", action="store_true", help="update the existing table instead of replacing it")
+    ap.add_argument("--only-missing", action="store_true", help="with --merge: tune only shapes not in the table")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import netops
@@ -141,6 +142,9 @@ def main():
     if a.merge and os.path.exists(base):
         table = {k: list(v) for k, v in json.load(open(base))["configs"].items()}
     tot_best = tot_model = 0.0
+    if a.only_missing:
+        uniq = {k: d for k, d in uniq.items() if k not in table}
+        print(f"{len(uniq)} shapes missing from the table", flush=True)
     for key, d in sorted(uniq.items()):
         best, us, res, model = tune_shape(d, dev, a.reps, a.cold)
         table[key] = list(best)

@@ -56,8 +56,8 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1) / a.reps
 
-    orig = {k: getattr(netops, k) for k in ("linear", "groupnorm", "layernorm", "attention_tc", "im2col",
-                                            "cast_f32_bf16", "latent_to_nhwc", "cfg_combine")}
+    orig = {k: getattr(netops, k) for k in ("linear", "groupnorm", "layernorm", "attention_tc", "attention_qkv",
+                                            "im2col", "cast_f32_bf16", "latent_to_nhwc", "cfg_combine")}
     noop = lambda *args, **kw: kw.get("out")            # noqa: E731
 
     def gemm_if(pred):
@@ -78,7 +78,7 @@ def main():
         ("GEMMs M<=512", {"linear": gemm_if(lambda M, N, K, kw: M <= 512)}),
         ("GroupNorm", {"groupnorm": noop}),
         ("LayerNorm", {"layernorm": noop}),
-        ("attention", {"attention_tc": noop}),
+        ("attention", {"attention_tc": noop, "attention_qkv": noop}),
         ("im2col/upsample/concat", {"im2col": noop}),
         ("cast f32->bf16", {"cast_f32_bf16": noop}),
     ]

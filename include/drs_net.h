@@ -133,6 +133,9 @@ int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N, int H, int
  * partial sums exchanged over DSMEM, input slice kept in shared memory);
  * workspace unused (may be NULL).  Otherwise two kernels (HW % 16 == 0) with
  * drs_groupnorm_workspace_bytes(N, G) bytes of workspace. */
+/* GroupNorm implementation switch (measurement): 0 auto (default), 1 one CTA per
+ * (image, group) with two L2 sweeps, 2 the cluster / two-kernel paths only. */
+int drs_set_gn_mode(int mode);
 int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int G, const float* gamma, const float* beta,
                   float eps, int silu, void* out, void* workspace, void* stream);
 size_t drs_groupnorm_workspace_bytes(int N, int G);

@@ -526,6 +526,115 @@ __global__ void gn_apply_kernel(const void* __restrict__ x, int x_f32, int HW, i
 // hardware cluster barrier every CTA sums the kGnCs partials of its groups
 // over DSMEM in rank order (bit-reproducible, no atomics, no workspace) and
 // applies (x - mean) * rstd * gamma + beta (+ SiLU) from shared memory.
+// ---- GroupNorm, one CTA per (image, group), two passes through L2 --------
+// The whole group (HW pixels x C/G channels) is reduced by one CTA: pass 1
+// sums (x - shift) and (x - shift)^2 in a fixed order (shift = the group's
+// first element: no cancellation when |mean| >> std), pass 2 re-reads the
+// (L2-resident) slice and writes silu(gamma (x - mean) rstd + beta).  No
+// cluster barrier or DSMEM exchange sits in the chain: one launch, two L2
+// sweeps.  Thread t owns channel pair (t % cp) of pixels t / cp, t / cp + P, ...
+// (cp = C / G / 2 pairs per pixel, P = blockDim / cp pixels per sweep).
+constexpr int kGnGroupThreads = 512;
+// auto: the group kernel only for small groups (its two L2 sweeps are latency-bound 4-byte
+// loads: tools/gn_bench.py, 2 x 64 x 1280: 3.9 vs 5.4 us cluster; 2 x 256 x 1280: 6.9 vs 6.6;
+// 2 x 4096 x 320: 26.7 vs 15.9)
+constexpr int64_t kGnGroupMaxElems = 4096;
+
+inline int& gn_mode() {          // drs_set_gn_mode: 0 auto, 1 group kernel, 2 cluster kernels only
+  static int m = 0;
+  return m;
+}
+
+template <bool F32>
+__device__ __forceinline__ float2 gn_ld2(const void* x, int64_t off) {
+  if constexpr (F32) return __ldg(reinterpret_cast<const float2*>(static_cast<const float*>(x) + off));
+  else return __bfloat1622float2(__ldg(reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(x) + off)));
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kGnGroupThreads)
+gn_group_kernel(const void* __restrict__ x, int HW, int C, int G, const float* __restrict__ gamma,
+                const float* __restrict__ beta, float eps, int silu, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[2][kGnGroupThreads / 32];
+  __shared__ float stat[2];
+  const int n = blockIdx.x / G, g = blockIdx.x - n * G;
+  const int cg = C / G, cp = cg >> 1;
+  const int P = blockDim.x / cp;                       // pixels per sweep
+  const int t = threadIdx.x;
+  const bool act = t < P * cp;
+  const int j = act ? t % cp : 0;
+  const int p0 = act ? t / cp : HW;
+  const int64_t base = (int64_t)n * HW * C + (int64_t)g * cg + 2 * j;
+  const float shift = gn_ld2<F32>(x, (int64_t)n * HW * C + (int64_t)g * cg).x;
+  float s = 0.f, q = 0.f;
+  constexpr int kU = 8;
+  for (int p = p0; p < HW; p += kU * P) {
+    float2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {                     // independent loads in flight
+      const int pp = p + u * P;
+      v[u] = pp < HW ? gn_ld2<F32>(x, base + (int64_t)pp * C) : make_float2(shift, shift);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const float a = v[u].x - shift, b = v[u].y - shift;
+      s += a + b;
+      q = fmaf(a, a, fmaf(b, b, q));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  const int warp = t >> 5, lane = t & 31;
+  if (lane == 0) { red[0][warp] = s; red[1][warp] = q; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? red[0][lane] : 0.f;
+    q = lane < nw ? red[1][lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if (lane == 0) {
+      const float cnt = (float)HW * (float)cg;
+      const float m = s / cnt;
+      stat[0] = shift + m;
+      stat[1] = rsqrtf(fmaxf(q / cnt - m * m, 0.f) + eps);
+    }
+  }
+  __syncthreads();
+  if (!act) return;
+  const float mean = stat[0], rstd = stat[1];
+  const int c = g * cg + 2 * j;
+  const float a0 = rstd * gamma[c], a1 = rstd * gamma[c + 1];
+  const float b0 = beta[c] - mean * a0, b1 = beta[c + 1] - mean * a1;
+  for (int p = p0; p < HW; p += kU * P) {
+    float2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pp = p + u * P;
+      v[u] = pp < HW ? gn_ld2<F32>(x, base + (int64_t)pp * C) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pp = p + u * P;
+      if (pp >= HW) break;
+      float y0 = fmaf(v[u].x, a0, b0), y1 = fmaf(v[u].y, a1, b1);
+      if (silu) {
+        y0 = y0 / (1.f + __expf(-y0));
+        y1 = y1 / (1.f + __expf(-y1));
+      }
+      *reinterpret_cast<__nv_bfloat162*>(out + base + (int64_t)pp * C) = __floats2bfloat162_rn(y0, y1);
+    }
+  }
+}
+
 constexpr int kGnCs = 8;                      // CTAs per cluster (portable size)
 
 __device__ __forceinline__ void gn_cluster_sync() {
@@ -1026,6 +1135,22 @@ extern "C" int drs_im2col(const void* x1, int C1, const void* x2, int C2, int N,
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+namespace drs {
+// (image, group) CTAs: chosen when every pair of channels sits in one group and
+// a group's slice is small enough that one SM sweeps it twice faster than the
+// cluster kernels' barrier chain (decided by tools/gn_bench.py A/B runs)
+static bool gn_group_ok(int N, int HW, int C, int G) {
+  const int cg = C / G;
+  return cg % 2 == 0 && cg / 2 <= kGnGroupThreads && (int64_t)HW * cg <= kGnGroupMaxElems;
+}
+}  // namespace drs
+
+extern "C" int drs_set_gn_mode(int mode) {
+  if (mode < 0 || mode > 2) return DRS_ERR_VALUE;
+  drs::gn_mode() = mode;
+  return DRS_OK;
+}
+
 extern "C" size_t drs_groupnorm_workspace_bytes(int N, int G) {
   return (size_t)(N > 0 ? N : 0) * (G > 0 ? G : 0) * drs::kGnSplit * sizeof(float2);   // two-kernel path only
 }
@@ -1035,6 +1160,16 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
   using namespace drs;
   if (N <= 0 || HW <= 0 || G <= 0 || C % G || (C / G) % 2 || !gamma || !beta) return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool al4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 3) == 0;
+  if (al4 && (C / G) % 2 == 0 && (gn_mode() == 1 || (gn_mode() == 0 && gn_group_ok(N, HW, C, G)))) {
+    if (x_f32)
+      launch_pdl(gn_group_kernel<true>, dim3(N * G), dim3(kGnGroupThreads), 0, st, x, HW, C, G, gamma, beta, eps,
+                 silu, static_cast<__nv_bfloat16*>(out));
+    else
+      launch_pdl(gn_group_kernel<false>, dim3(N * G), dim3(kGnGroupThreads), 0, st, x, HW, C, G, gamma, beta, eps,
+                 silu, static_cast<__nv_bfloat16*>(out));
+    return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+  }
   int gpc, rpc, threads, keep;
   size_t smem;
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;

@@ -186,11 +186,14 @@ def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d, amp):
                                                (2, 64, 1280, 32, False, True), (16, 4096, 320, 32, False, True),
                                                (2, 16384, 320, 32, False, False), (3, 100, 960, 32, False, True),
                                                (2, 256, 64, 32, False, True)])
-def test_groupnorm(cuda, N, HW, C, G, f32, silu):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_groupnorm(cuda, N, HW, C, G, f32, silu, mode):
     """GroupNorm (+SiLU) vs torch fp32: fused cooperative path (slice kept in smem
     or re-read), the two-kernel fallback (C/G < 8), bit-identical repeats, and
     replays from a CUDA graph (grid-barrier state reused across launches)."""
+    from paper_2603_25872_b200 import _lib
     from paper_2603_25872_b200.netops import groupnorm
+    _lib.lib().drs_set_gn_mode(mode)          # 1: one CTA per (image, group); 2: cluster / two-kernel paths
     g = torch.Generator(device=cuda).manual_seed(N * HW + C)
     x = (torch.randn(N * HW, C, device=cuda, generator=g) * 2 + 0.5)
     x = x if f32 else x.bfloat16()
@@ -217,6 +220,7 @@ def test_groupnorm(cuda, N, HW, C, G, f32, silu):
         gr.replay()
         gr.replay()
     torch.cuda.synchronize()
+    _lib.lib().drs_set_gn_mode(0)
     assert torch.equal(out, out2)
 
 

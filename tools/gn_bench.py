@@ -24,7 +24,8 @@ def main():
                        (16, 4096, 320)]:
         G = 32
         line = []
-        for fused in (True, False):
+        for mode, fused in ((1, True), (2, True), (2, False)):
+            _lib.lib().drs_set_gn_mode(mode)
             raw = torch.randn(N * HW * C + 8, device=dev).bfloat16()
             x = raw[:N * HW * C].view(N * HW, C) if fused else raw[4:4 + N * HW * C].view(N * HW, C)
             gamma, beta = torch.randn(C, device=dev), torch.randn(C, device=dev)
@@ -47,7 +48,8 @@ def main():
                 torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / 200
             mb = 2 * N * HW * C * 2 / 1e6
-            line.append(f"{'fused' if fused else '2-kern'} {us:6.2f} us ({mb / us:5.2f} TB/s)")
+            name = "group" if mode == 1 else ("cluster" if fused else "2-kern")
+            line.append(f"{name} {us:6.2f} us ({mb / us:5.2f} TB/s)")
         print(f"N={N:2d} HW={HW:5d} C={C:4d}: " + "   ".join(line))
 
 

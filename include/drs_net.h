@@ -115,6 +115,14 @@ int drs_attention_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, con
 int drs_attention_tc_v(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                        void* o, int64_t ldo, int B, int H, int Lq, int Lk, int d, float scale, void* stream);
 
+/* GEMV for M <= 4 rows: out[m, n] = act(x[m, :] . w[n, :] + bias[n]) (+ res[m, n]),
+ * act DRS_ACT_NONE / DRS_ACT_SILU, bf16 x / w (K % 8 == 0, w 16-byte aligned),
+ * fp32 or bf16 residual / output.  HBM-bound weight stream on the CUDA cores
+ * (the conditioning MLPs of the denoisers: timestep and adaLN embeddings). */
+int drs_gemv(const void* x, int64_t ldx, const void* w, int64_t ldw, const float* bias, const void* res,
+             int64_t ldr, int res_f32, void* out, int64_t ldo, int out_f32, int M, int N, int K, int act,
+             int ctas_per_sm /* 0: 4 per SM; 1: leaves room for co-resident GEMM CTAs */, void* stream);
+
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);
 int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out_bf16, void* stream);

@@ -1115,6 +1115,129 @@ extern "C" int drs_unpatchify(const float* tok, int Cout, int Ckeep, int H, int 
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
+namespace drs {
+// ---- GEMV for M <= 4 rows (conditioning MLPs: timestep / adaLN embeddings) ----
+// y[m, n] = act(sum_k x[m, k] W[n, k] + bias[n]) (+ residual[m, n]).  The weight
+// stream is the whole cost (DiT adaLN: 446 MB for one row): each warp owns rows
+// n, reads them with 16-byte ld.global.nc (L1 no-allocate) loads, kGvRows rows in
+// flight per lane, the x rows sit in shared memory as fp32; a small-footprint CTA
+// (256 threads, <= 72 KB smem) that co-resides with the tensor-core GEMMs, so the
+// conditioning GEMVs can run on a side stream under them.
+constexpr int kGvThreads = 256;
+constexpr int kGvRows = 4;          // weight rows per warp in flight
+constexpr int kGvMaxM = 4;
+
+__device__ __forceinline__ uint4 ld_nc_na_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+template <int MM>
+__global__ void __launch_bounds__(kGvThreads)
+gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat16* __restrict__ w, int64_t ldw,
+            const float* __restrict__ bias, const void* __restrict__ res, int64_t ldr, int res_f32,
+            void* __restrict__ out, int64_t ldo, int out_f32, int N, int K, int act) {
+  extern __shared__ uint4 sx[];                       // [MM][K / 8] bf16 x 8
+  pdl_wait();
+  pdl_trigger();
+  const int kv = K >> 3;                              // 16-byte vectors per row
+  for (int i = threadIdx.x; i < MM * kv; i += blockDim.x) {
+    const int m = i / kv, k = i - m * kv;
+    sx[i] = *reinterpret_cast<const uint4*>(x + (int64_t)m * ldx + 8 * k);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * (kGvThreads / 32);
+  const int wid = blockIdx.x * (kGvThreads / 32) + (threadIdx.x >> 5);
+  for (int n0 = wid * kGvRows; n0 < N; n0 += warps_total * kGvRows) {
+    float acc[kGvRows][MM];
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r)
+#pragma unroll
+      for (int m = 0; m < MM; ++m) acc[r][m] = 0.f;
+    for (int v = lane; v < kv; v += 32) {
+      uint4 wv[kGvRows];
+#pragma unroll
+      for (int r = 0; r < kGvRows; ++r)               // rows of this warp: independent loads in flight
+        wv[r] = n0 + r < N ? ld_nc_na_v4(w + (int64_t)(n0 + r) * ldw + 8 * v) : make_uint4(0, 0, 0, 0);
+      float2 xf[MM][4];                                // x[m, 8v .. 8v+7] (conflict-free 16-byte reads)
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const uint4 xv = sx[m * kv + v];
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xf[m][e] = __bfloat1622float2(xh[e]);
+      }
+#pragma unroll
+      for (int r = 0; r < kGvRows; ++r) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&wv[r]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+#pragma unroll
+          for (int m = 0; m < MM; ++m) acc[r][m] = fmaf(f.x, xf[m][e].x, fmaf(f.y, xf[m][e].y, acc[r][m]));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r)
+#pragma unroll
+      for (int m = 0; m < MM; ++m)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc[r][m] += __shfl_xor_sync(0xffffffffu, acc[r][m], o);
+    if (lane < kGvRows * MM) {                        // lane (r, m) finishes output (m, n0 + r)
+      const int r = lane / MM, m = lane - r * MM;
+      float y = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < kGvRows; ++rr)
+#pragma unroll
+        for (int mm = 0; mm < MM; ++mm)
+          if (rr == r && mm == m) y = acc[rr][mm];
+      const int n = n0 + r;
+      if (n < N) {
+        if (bias) y += bias[n];
+        if (act == DRS_ACT_SILU) y = y / (1.f + __expf(-y));
+        if (res) y += res_f32 ? static_cast<const float*>(res)[(int64_t)m * ldr + n]
+                              : __bfloat162float(static_cast<const __nv_bfloat16*>(res)[(int64_t)m * ldr + n]);
+        if (out_f32) static_cast<float*>(out)[(int64_t)m * ldo + n] = y;
+        else static_cast<__nv_bfloat16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16(y);
+      }
+    }
+  }
+}
+}  // namespace drs
+
+extern "C" int drs_gemv(const void* x, int64_t ldx, const void* w, int64_t ldw, const float* bias, const void* res,
+                        int64_t ldr, int res_f32, void* out, int64_t ldo, int out_f32, int M, int N, int K, int act,
+                        int ctas_per_sm, void* stream) {
+  using namespace drs;
+  if (M < 1 || M > kGvMaxM || N < 1 || K < 8 || K % 8 || ldw % 8 || ldx % 8 || !x || !w || !out) return DRS_ERR_VALUE;
+  if (act != DRS_ACT_NONE && act != DRS_ACT_SILU) return DRS_ERR_VALUE;
+  if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(x)) & 15) return DRS_ERR_VALUE;
+  const size_t smem = (size_t)M * K * 2;
+  if (smem > 72 * 1024) return DRS_ERR_VALUE;
+  static int sms = [] { int d = 0, n = 148; cudaGetDevice(&d); cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d); return n; }();
+  const int warps_needed = (N + kGvRows - 1) / kGvRows;
+  int blocks = (warps_needed + kGvThreads / 32 - 1) / (kGvThreads / 32);
+  const int cps = ctas_per_sm > 0 ? ctas_per_sm : 4;      // 1: leave room for co-resident GEMMs
+  if (blocks > cps * sms) blocks = cps * sms;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kern, dim3(blocks), dim3(kGvThreads), smem, st, static_cast<const __nv_bfloat16*>(x), ldx,
+               static_cast<const __nv_bfloat16*>(w), ldw, bias, res, ldr, res_f32, out, ldo, out_f32, N, K, act);
+  };
+  switch (M) {
+    case 1: go(gemv_kernel<1>); break;
+    case 2: go(gemv_kernel<2>); break;
+    case 3: go(gemv_kernel<3>); break;
+    default: go(gemv_kernel<4>); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
 extern "C" int drs_silu_cast(const float* x, int64_t n, void* out, void* stream) {
   if (n < 0) return DRS_ERR_VALUE;
   if (n == 0) return DRS_OK;

@@ -121,6 +121,8 @@ class DiT:
         # one fused QKV GEMM; the attention reads V row-major as an MN-major operand
         # (DRS_QKV_FUSED=0: Q|K GEMM + swapped V^T GEMM, the round-1 layout)
         self.fused_qkv = os.environ.get("DRS_QKV_FUSED", "1") != "0"
+        self.overlap_mod = os.environ.get("DRS_DIT_OVERLAP", "0") == "1" and self.device.type == "cuda"
+        self._side = torch.cuda.Stream(self.device) if self.overlap_mod else None
         self.qkv = torch.empty(MB, 3 * h, dtype=bf, device=dev)            # Q | K | V
         self.vt = torch.empty(h, MB, dtype=bf, device=dev)                 # V^T (unfused layout only)
         self.att = torch.empty(MB, h, dtype=bf, device=dev)
@@ -135,6 +137,39 @@ class DiT:
         self.mod = torch.empty(max_batch, L * 6 * h, dtype=f32, device=dev)
         self.fmod = torch.empty(max_batch, 2 * h, dtype=f32, device=dev)
         self.eps_img = torch.empty(max_batch, cfg.in_ch, cfg.input_size, cfg.input_size, dtype=f32, device=dev)
+
+    # DRS_DIT_OVERLAP=1 (measured slower, off by default): the adaLN modulation GEMVs
+    # (M = B rows, 6 h columns per block, 446 MB of weights for 28 blocks) in chunks on a
+    # side stream, each block waiting only for its own chunk.  On a B200 the side stream's
+    # weight stream slows the blocks' latency-bound GEMMs more than it hides
+    # (DiT b1 1.565 -> 1.63 ms with one GEMV CTA per SM; no change with four), so the
+    # default keeps one in-line GEMV at the head of the eval.
+    MOD_CHUNKS = ((0, 1), (1, 2), (2, 4), (4, 8), (8, 28))
+
+    def _modulations(self, B):
+        w, h, L = self.w, self.cfg.hidden, self.cfg.depth
+        if not self.overlap_mod:
+            ops.linear(self.c_act[:B], w.ada_w, bias=w.ada_b, out=self.mod[:B])
+            ops.linear(self.c_act[:B], w.f_ada_w, bias=w.f_ada_b, out=self.fmod[:B])
+            return {}
+        main = torch.cuda.current_stream(self.device)
+        self._side.wait_stream(main)                 # c_act is ready
+        ready = {}
+        with torch.cuda.stream(self._side):
+            for l0, l1 in self.MOD_CHUNKS:
+                if l0 >= L:
+                    break
+                l1 = min(l1, L)
+                a, b = l0 * 6 * h, l1 * 6 * h
+                ops.linear(self.c_act[:B], w.ada_w[a:b], bias=w.ada_b[a:b], out=self.mod[:B, a:b], gemv_ctas=1)
+                ev = torch.cuda.Event()
+                ev.record(self._side)
+                ready[l0] = ev
+            ops.linear(self.c_act[:B], w.f_ada_w, bias=w.f_ada_b, out=self.fmod[:B], gemv_ctas=1)
+            ev = torch.cuda.Event()
+            ev.record(self._side)
+            ready["final"] = ev
+        return ready
 
     def forward(self, xs, t_dev, B: int, outs=None):
         """xs: list of B latents (in_ch*S*S, fp64/fp32 CUDA tensors); t_dev: (>=B,) fp32 device
@@ -152,10 +187,12 @@ class DiT:
         ops.linear(self.t_freq[:B], w.t_w1, bias=w.t_b1, act="silu", out=self.t_h[:B])
         ops.linear(self.t_h[:B], w.t_w2, bias=w.t_b2, residual=self.y_emb[:B], out=self.c[:B])
         ops.silu_cast(self.c[:B], self.c_act[:B])
-        ops.linear(self.c_act[:B], w.ada_w, bias=w.ada_b, out=self.mod[:B])
-        ops.linear(self.c_act[:B], w.f_ada_w, bias=w.f_ada_b, out=self.fmod[:B])
+        ready = self._modulations(B)
         hs, xn, qkv, att, mlp = self.hs[:M], self.xn[:M], self.qkv[:M], self.att[:M], self.mlp[:M]
+        main = torch.cuda.current_stream(self.device)
         for i, blk in enumerate(w.blocks):
+            if i in ready:
+                main.wait_event(ready[i])
             base = i * 6 * h
             md = self.mod[:B]
             sh_a, sc_a, g_a = md[:, base:base + h], md[:, base + h:base + 2 * h], md[:, base + 2 * h:base + 3 * h]
@@ -179,6 +216,9 @@ class DiT:
             ops.layernorm(hs, out=xn, shift=sh_m, scale=sc_m, eps=1e-6, mod_group=T)
             ops.linear(xn, blk["fc1_w"], bias=blk["fc1_b"], act="gelu_tanh", out=mlp)
             ops.linear(mlp, blk["fc2_w"], bias=blk["fc2_b"], colscale=g_m, cs_group=T, residual=hs, out=hs)
+        if "final" in ready:
+            main.wait_event(ready["final"])
+            main.wait_stream(self._side)            # join the side stream (graph capture needs it)
         fm = self.fmod[:B]
         ops.layernorm(hs, out=xn, shift=fm[:, 0:h], scale=fm[:, h:2 * h], eps=1e-6, mod_group=T)
         ops.linear(xn, w.f_w, bias=w.f_b, out=self.tout[:M])

@@ -26,7 +26,7 @@ def _ptr(t):
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
            bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None,
-           b_img=None, hs_valid=0, out2=None):
+           b_img=None, hs_valid=0, out2=None, gemv_ctas=0):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group.  b_img = (rows, off): rows
@@ -35,6 +35,9 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     96-column head, softmax (exp2) over the first hs_valid columns.  out2: a bf16
     tensor that also receives the (fp32) output, rounded."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+    if (conv is None and x.shape[0] <= 4 and act in (None, "none", "silu") and colscale is None and rowbias is None
+            and b_img is None and out2 is None and GEMV and _gemv_ok(x, w)):
+        return gemv(x, w, bias=bias, act=act, residual=residual, out=out, out_dtype=out_dtype, ctas_per_sm=gemv_ctas)
     if conv is not None:          # implicit 3x3 conv: x is NHWC (N*H*W, C), K = 9*C
         cn, ch, cw, cc = conv
         M, K = cn * ch * cw, 9 * cc
@@ -90,6 +93,34 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     if TIMERS is not None:
         e1.record()
         TIMERS.append((2.0 * M * N * K, e0, e1, (M, N, K, bn, split)))
+    return out
+
+
+# M <= 4 linears (the conditioning MLPs) run on the CUDA-core GEMV (drs_gemv): a
+# pure weight stream, small enough to co-reside with the tensor-core GEMMs
+GEMV = os.environ.get("DRS_GEMV", "1") != "0"
+
+
+def _gemv_ok(x, w):
+    K = x.shape[1]
+    return (K % 8 == 0 and x.stride(1) == 1 and w.stride(1) == 1 and x.stride(0) % 8 == 0 and w.stride(0) % 8 == 0
+            and x.data_ptr() % 16 == 0 and w.data_ptr() % 16 == 0 and x.shape[0] * K * 2 <= 72 * 1024)
+
+
+def gemv(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, ctas_per_sm=0):
+    """out[m, n] = act(x[m] . w[n] + bias[n]) (+ residual[m, n]) for M <= 4 rows (drs_gemv).
+    ctas_per_sm=1 keeps the grid small enough for tensor-core GEMM CTAs to co-reside
+    (side-stream use); 0 = 4 CTAs per SM (in-line use)."""
+    M, K = x.shape
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty(M, N, dtype=out_dtype, device=x.device)
+    st = _lib.lib().drs_gemv(x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), _ptr(bias), _ptr(residual),
+                             residual.stride(0) if residual is not None else 0,
+                             int(residual is not None and residual.dtype == torch.float32), out.data_ptr(),
+                             out.stride(0), int(out.dtype == torch.float32), M, N, K, ACT[act], int(ctas_per_sm),
+                             _lib.stream_ptr())
+    _lib.check(st, "drs_gemv")
     return out
 
 

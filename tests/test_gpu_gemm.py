@@ -246,3 +246,31 @@ def test_gemm_bf16_copy_output(cuda, M, N, K, bn, split, pair):
     linear(x, w, bias=b, residual=s, out=s, out2=cp, bn=bn, split=split, pair=pair)
     assert (s - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
     assert torch.equal(cp, s.bfloat16())
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1152, 1152), (1, 193536, 1152), (2, 1280, 320), (1, 20160, 1280),
+                                   (3, 77, 264), (4, 2304, 4608), (2, 5, 16)])
+@pytest.mark.parametrize("act,res,out_f32", [(None, None, True), ("silu", None, False), (None, "f32", True),
+                                             ("silu", "bf16", False)])
+def test_gemv_small_m(cuda, M, N, K, act, res, out_f32):
+    """M <= 4 linears dispatch to the CUDA-core GEMV (drs_gemv) -- vs torch fp32."""
+    from paper_2603_25872_b200.netops import gemv, linear
+    g = torch.Generator(device=cuda).manual_seed(M * N + K)
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g)
+    r = None
+    if res:
+        r = torch.randn(M, N, device=cuda, generator=g)
+        r = r if res == "f32" else r.bfloat16()
+    ref = x.float() @ w.float().t() + bias
+    if act == "silu":
+        ref = torch.nn.functional.silu(ref)
+    if r is not None:
+        ref = ref + r.float()
+    dt = torch.float32 if out_f32 else torch.bfloat16
+    for fn in (gemv, linear):
+        y = fn(x, w, bias=bias, act=act, residual=r, out_dtype=dt)
+        assert y.dtype == dt
+        err = (y.float() - ref).abs().max().item()
+        assert err <= (1e-3 if out_f32 else 1e-2) * max(1.0, ref.abs().max().item()), (fn.__name__, err)

@@ -123,6 +123,9 @@ int drs_gemv(const void* x, int64_t ldx, const void* w, int64_t ldw, const float
              int64_t ldr, int res_f32, void* out, int64_t ldo, int out_f32, int M, int N, int K, int act,
              int ctas_per_sm /* 0: 4 per SM; 1: leaves room for co-resident GEMM CTAs */, void* stream);
 
+/* Measurement switch: 1 (default) = attention with separate S and PV MMA issuer warps, 0 = one. */
+int drs_set_attn_split(int on);
+
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);
 int drs_patchify(const void* x, int x_f64, int C, int H, int W, int p, void* out_bf16, void* stream);

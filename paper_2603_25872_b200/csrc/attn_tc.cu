@@ -160,8 +160,11 @@ __device__ __forceinline__ int sw128_off(int row, int c) {
 // VROW: V given row-major (keys x channels, the V block of a fused QKV GEMM
 // output) and loaded exactly like K; the PV MMA reads it as an MN-major B
 // operand (b_major = 1) -- no separate V^T GEMM.  Otherwise V^T (channels x keys).
-template <int DP, int NPOLY, bool VROW>
-__global__ void __launch_bounds__(kAttnTcThreads, 1)
+// SPLIT: a second MMA warp (warp 10) issues the PV MMAs while warp 1 issues only
+// the S MMAs, so S_{j+2} no longer waits in warp 1's program order behind P_j
+// (ncu: the softmax warps spent 21.5 % of their samples waiting for S tiles).
+template <int DP, int NPOLY, bool VROW, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? kAttnTcThreads + 32 : kAttnTcThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
                int Lq, int Lk, int d, int vt_img, float scale_log2) {
@@ -278,6 +281,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         tc::mbar_wait(&s_free[j & 1], (j >> 1) & 1);
         issue_s(j + 2);
       }
+      if constexpr (SPLIT) continue;           // PV MMAs: warp 10
       tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
       const int st = j % kSt;
       tc::mbar_wait(&v_full[st], (j / kSt) & 1);
@@ -289,6 +293,27 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
         for (int kk = 0; kk < kAK / 16; ++kk) {
           // VROW: 16 keys = 16 rows of 128 B per K step; channel atoms kAK * 128 B apart
+          const uint64_t bdesc = VROW ? tc::smem_desc_sw128_mn(vb + kk * 2048, kAK * 128) : kdesc(vb, kk, DP * 128);
+          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), bdesc,
+                       kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(&v_empty[st]);
+        tc::mma_commit(&o_done[j & 1]);
+      }
+      __syncwarp();
+    }
+  } else if (SPLIT && warp == 10) {
+    // PV issuer: O_set += P_j V_j as soon as P_j is published and V_j landed
+    for (int j = 0; j < n_tiles; ++j) {
+      tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      const int st = j % kSt;
+      tc::mbar_wait(&v_full[st], (j / kSt) & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint8_t* vb = sV + st * S::kVBytes;
+        const uint32_t o_col = 256 + (kSets == 2 ? (j & 1) * DP : 0);
+#pragma unroll
+        for (int kk = 0; kk < kAK / 16; ++kk) {
           const uint64_t bdesc = VROW ? tc::smem_desc_sw128_mn(vb + kk * 2048, kAK * 128) : kdesc(vb, kk, DP * 128);
           tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), bdesc,
                        kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
@@ -544,11 +569,11 @@ static bool tmap_vt(CUtensorMap* m, const void* ptr, int64_t chans, int64_t keys
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DP, int NPOLY, bool VROW>
+template <int DP, int NPOLY, bool VROW, bool SPLIT>
 static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                          int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   using S = AttnSmem<DP>;
-  auto kern = attn_tc_kernel<DP, NPOLY, VROW>;
+  auto kern = attn_tc_kernel<DP, NPOLY, VROW, SPLIT>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
@@ -556,17 +581,26 @@ static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
     attr = true;
   }
   dim3 grid((Lq + kAQ - 1) / kAQ, H, B);
-  launch_pdl(kern, dim3(grid), dim3(kAttnTcThreads), S::kBytes, st, tq, tk, tv, to, Lq, Lk, d, vt_img, sl2);
+  launch_pdl(kern, dim3(grid), dim3(SPLIT ? kAttnTcThreads + 32 : kAttnTcThreads), S::kBytes, st, tq, tk, tv, to,
+             Lq, Lk, d, vt_img, sl2);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+// drs_set_attn_split: 1 = separate S / PV MMA issuer warps (SPLIT), 0 = one MMA warp
+inline int& attn_split_mma() {
+  static int on = 1;
+  return on;
 }
 
 template <int DP, bool VROW>
 static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                        int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   static int npoly = [] { const char* e = getenv("DRS_ATTN_POLY"); return e ? atoi(e) : 2; }();
-  if (npoly == 0) return launch_attn_v<DP, 0, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  if (npoly == 3) return launch_attn_v<DP, 3, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  return launch_attn_v<DP, 2, VROW>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (attn_split_mma())
+    return launch_attn_v<DP, 2, VROW, true>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (npoly == 0) return launch_attn_v<DP, 0, VROW, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  if (npoly == 3) return launch_attn_v<DP, 3, VROW, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
+  return launch_attn_v<DP, 2, VROW, false>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
 }
 
 }  // namespace drs
@@ -616,4 +650,9 @@ extern "C" int drs_attention_tc_v(const void* q, int64_t ldq, const void* k, int
 
 extern "C" int drs_attention_tc_debug(int* mapped_trace) {
   return cudaMemcpyToSymbol(drs::g_attn_trace, &mapped_trace, sizeof(int*)) == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_set_attn_split(int on) {
+  drs::attn_split_mma() = on ? 1 : 0;
+  return DRS_OK;
 }

@@ -31,9 +31,11 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--only", default="", help="substring of the shape label to run")
     ap.add_argument("--eager", type=int, default=0, help="N eager launches only (for ncu), no timing")
+    ap.add_argument("--split", type=int, default=1, help="separate S / PV MMA issuer warps (1) or one (0)")
     a = ap.parse_args()
     import torch
-    from paper_2603_25872_b200 import netops
+    from paper_2603_25872_b200 import _lib, netops
+    _lib.lib().drs_set_attn_split(a.split)
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     for label, B, H, Lq, Lk, d in SHAPES:

@@ -76,6 +76,10 @@ typedef struct drs_gemm_args {
    * out2[m, n] = bf16(C[m, n]), row stride ldo2 (the transformer's residual stream
    * and the bf16 input of the projection that follows, in one epilogue). */
   void* out2; int64_t ldo2;
+  /* implicit conv stride: 0 / 1, or 2 (conv_H / conv_W are then the OUTPUT grid of
+   * a stride-2, pad-1 3x3 conv over a 2H x 2W input; the A box is loaded with TMA
+   * element stride 2 -- downsamplers without an im2col copy). */
+  int conv_stride;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
 

@@ -78,10 +78,11 @@ class DrsGemmArgs(ctypes.Structure):       # include/drs_net.h drs_gemm_args
         ("cta_pair", ctypes.c_int),
         ("b_img_rows", ctypes.c_int), ("b_img_off", ctypes.c_int), ("hs_valid", ctypes.c_int),
         ("out2", ctypes.c_void_p), ("ldo2", ctypes.c_int64),
+        ("conv_stride", ctypes.c_int),
     ]
 
 
-assert ctypes.sizeof(DrsGemmArgs) == 216
+assert ctypes.sizeof(DrsGemmArgs) == 224
 assert ctypes.sizeof(DrsKey) == 48
 assert ctypes.sizeof(DrsOp) == 112
 

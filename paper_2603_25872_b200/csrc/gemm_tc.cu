@@ -434,7 +434,7 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 // Implicit-GEMM 3x3 convolution (stride 1, pad 1) over an NHWC bf16 input:
 // A[(n,y,x), (ky,kx,c)] is never materialised -- the k-block (tap, 64-channel
 // block) of a 128-pixel tile is ONE 4-D TMA box {64 ch, W, rows, images} of
-// the input at (c0, x0 + kx - 1, y0 + ky - 1, n0); TMA zero-fills the
+// the input at (c0, x0 + kx - 1, y0 * cv.stride + ky - 1, n0); TMA zero-fills the
 // out-of-image taps, which is exactly the zero padding.
 struct ConvGeom {
   int on;          // 0: plain GEMM (2-D A map)
@@ -442,6 +442,8 @@ struct ConvGeom {
   int H, W;        // image size (W <= 128, W * rows * imgs == 128 pixels per tile)
   int b_img_rows;  // > 0: tiles whose first row m has (m / b_img_rows) odd read B rows + b_img_off
   int b_img_off;
+  int stride;      // 1, or 2 (H, W are then the OUTPUT grid; the TMA box walks the input with
+                   // element stride 2, so input row = 2 y + ky - 1: no im2col for downsamplers)
 };
 
 __device__ __forceinline__ int b_row_offset(const ConvGeom& cv, int m0) {
@@ -609,7 +611,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
             const int ky = tap / 3, kx = tap - ky * 3;
             const int m0 = mt * kBM, hw = cv.H * cv.W;
             const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-            tma_load_4d(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+            tma_load_4d(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
           } else {
             tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
           }
@@ -922,7 +924,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
             const int ky = tap / 3, kx = tap - ky * 3;
             const int hw = cv.H * cv.W;
             const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-            tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+            tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
           } else {
             tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
           }
@@ -1122,7 +1124,7 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           const int ky = tap / 3, kx = tap - ky * 3;
           const int hw = cv.H * cv.W;
           const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-          tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 + ky - 1, n0);
+          tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
         } else {
           tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
         }
@@ -1245,15 +1247,19 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
 }
 
 // NHWC input as {C, W, H, N}; box {64 ch, W, rows, imgs} with W * rows * imgs == 128
-static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C) {
+// H, W: the OUTPUT grid; the input is (s H) x (s W).  With s = 2 the box spans
+// 2 W x 2 rows input elements traversed with element stride 2, i.e. it loads the
+// same 128 x 64-channel tile of pixels (s y + ky - 1, s x + kx - 1).
+static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
   const int rows = W >= 128 ? 1 : (128 / W <= H ? 128 / W : H);
   const int imgs = 128 / (W * rows);
-  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)rows, (cuuint32_t)imgs};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const int Hi = H * s, Wi = W * s;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)Wi, (cuuint64_t)Hi, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)Wi * C * 2, (cuuint64_t)Hi * Wi * C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)(W * s), (cuuint32_t)(rows * s), (cuuint32_t)imgs};
+  cuuint32_t estr[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -1551,7 +1557,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (split < 0 || split > 8) return DRS_ERR_VALUE;            // portable cluster size
   if (bn == 0 || split == 0) gemm_auto_config(M, N, K, bn, split);
   CUtensorMap ta, tb;
-  ConvGeom cv{0, 0, 0, 0, 0, 0};
+  ConvGeom cv{0, 0, 0, 0, 0, 0, 1};
   const bool hsm = g->act == DRS_ACT_HEADSOFTMAX;
   if (hsm) {
     if (g->out_f32 || N % 96 || g->hs_valid <= 0 || g->hs_valid > 96 || (g->ldc % 8) ||
@@ -1563,12 +1569,14 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (g->b_img_rows > 0 && (g->b_img_rows % kBM || g->b_img_off <= 0)) return DRS_ERR_VALUE;
   if (g->conv_C > 0) {      // implicit 3x3 conv: A = NHWC input, M = N*H*W, K = 9*C
     const int C = g->conv_C, H = g->conv_H, W = g->conv_W, Nimg = g->conv_N;
+    const int cs = g->conv_stride > 1 ? g->conv_stride : 1;
+    if (cs > 2 || (cs == 2 && W * 2 > 256)) return DRS_ERR_VALUE;
     if (C % 64 || W > 128 || (W & (W - 1)) || (int64_t)Nimg * H * W != M || K != 9 * C) return DRS_ERR_VALUE;
     const int rows = W >= 128 ? 1 : (128 / W <= H ? 128 / W : H);
     if (W * rows * (128 / (W * rows)) != 128 || H % rows || (128 / (W * rows) > 1 && (rows != H || Nimg % (128 / (W * H)))))
       return DRS_ERR_VALUE;
-    if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C)) return DRS_ERR_CUDA;
-    cv = ConvGeom{1, C / 64, H, W, 0, 0};
+    if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C, cs)) return DRS_ERR_CUDA;
+    cv = ConvGeom{1, C / 64, H, W, 0, 0, cs};
   } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
     return DRS_ERR_CUDA;
   }

@@ -38,8 +38,8 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
     if (conv is None and x.shape[0] <= 4 and act in (None, "none", "silu") and colscale is None and rowbias is None
             and b_img is None and out2 is None and GEMV and _gemv_ok(x, w)):
         return gemv(x, w, bias=bias, act=act, residual=residual, out=out, out_dtype=out_dtype, ctas_per_sm=gemv_ctas)
-    if conv is not None:          # implicit 3x3 conv: x is NHWC (N*H*W, C), K = 9*C
-        cn, ch, cw, cc = conv
+    if conv is not None:          # implicit 3x3 conv: x is NHWC, K = 9*C; conv = (N, H, W, C[, stride])
+        cn, ch, cw, cc = conv[:4]   # H, W: the output grid (input 2H x 2W for stride 2)
         M, K = cn * ch * cw, 9 * cc
     else:
         M, K = x.shape
@@ -71,13 +71,14 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
         SHAPES.append((M, N, K, act, residual is not None and residual.dtype == torch.float32,
                        residual is not None, out.dtype == torch.float32, None if conv is None else tuple(conv)))
     if bn == 0 or split == 0:                    # tuned table, else the library cost model
-        bn, split, tpair = pick3(M, N, K, bn, split, conv is not None)
+        bn, split, tpair = pick3(M, N, K, bn, split, False if conv is None else (conv[4] if len(conv) > 4 else 1))
         if pair is None:
             pair = tpair
     g.bn, g.split = bn, split
     g.cta_pair = 1 if pair else 0
     if conv is not None:
-        g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv
+        g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv[:4]
+        g.conv_stride = conv[4] if len(conv) > 4 else 1
     if b_img is not None:
         g.b_img_rows, g.b_img_off = b_img
     g.hs_valid = hs_valid
@@ -146,7 +147,8 @@ def _table():
 
 
 def table_key(M, N, K, conv=False):
-    return f"{M}x{N}x{K}" + (":conv" if conv else "")
+    """conv: False, True / 1 (stride-1 implicit conv) or 2 (stride-2)."""
+    return f"{M}x{N}x{K}" + ((":conv2" if conv == 2 else ":conv") if conv else "")
 
 
 def pick3(M, N, K, bn=0, split=0, conv=False):

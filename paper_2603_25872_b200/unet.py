@@ -85,6 +85,8 @@ class UNet:
         # self-attention Q, K, V from ONE GEMM; the attention kernel reads V row-major
         # (DRS_QKV_FUSED=0: Q|K GEMM + swapped V^T GEMM, the round-1 layout)
         self.fused_qkv = os.environ.get("DRS_QKV_FUSED", "1") != "0"
+        # stride-2 downsampling convs as implicit GEMMs (DRS_STRIDED_CONV=0: im2col + GEMM)
+        self.strided_conv = os.environ.get("DRS_STRIDED_CONV", "1") != "0"
         I = _Init(self.device, seed)
         c0, T = cfg.channels[0], cfg.temb_dim
         self.p = p = {}
@@ -231,6 +233,12 @@ class UNet:
         GEMMs (A tiles are 4-D TMA boxes of the input; no im2col); a nearest-2x
         upsample is materialised first (4x, vs 9x for im2col); the stride-2
         downsamples go through im2col."""
+        if x2 is None and stride == 2 and self.strided_conv and ops.implicit_conv_ok(N, H // 2, W // 2, c1):
+            # downsampler: the TMA box walks the input with element stride 2 (no im2col)
+            Ho, Wo = H // 2, W // 2
+            if self._count:
+                self.flops += 2.0 * N * Ho * Wo * wb[0].shape[0] * wb[0].shape[1]
+            return ops.linear(x1, wb[0], bias=wb[1], conv=(N, Ho, Wo, c1, 2), **kw), Ho, Wo
         if x2 is None and stride == 1 and ops.implicit_conv_ok(N, H * up, W * up, c1):
             if up == 2:
                 xu = self.buf(f"ups{c1}_{H}", (N * 4 * H * W, c1))

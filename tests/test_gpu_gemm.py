@@ -274,3 +274,26 @@ def test_gemv_small_m(cuda, M, N, K, act, res, out_f32):
         assert y.dtype == dt
         err = (y.float() - ref).abs().max().item()
         assert err <= (1e-3 if out_f32 else 1e-2) * max(1.0, ref.abs().max().item()), (fn.__name__, err)
+
+
+@pytest.mark.parametrize("N,H,W,C,Co", [(2, 32, 32, 320, 320), (2, 16, 16, 640, 640), (2, 8, 8, 1280, 1280),
+                                        (1, 64, 64, 128, 192)])
+@pytest.mark.parametrize("bn,split,pair", [(0, 0, None), (128, 1, False), (64, 3, False), (128, 1, True)])
+def test_implicit_conv3x3_stride2(cuda, N, H, W, C, Co, bn, split, pair):
+    """Stride-2 3x3 conv (the UNet downsamplers) as an implicit GEMM: the TMA box
+    walks the NHWC input with element stride 2 -- vs torch conv2d(stride=2, pad=1)."""
+    from paper_2603_25872_b200.netops import implicit_conv_ok, linear
+    Ho, Wo = H // 2, W // 2
+    if not implicit_conv_ok(N, Ho, Wo, C) or (pair and N * Ho * Wo < 256):
+        pytest.skip("geometry not covered by the implicit path")
+    g = torch.Generator(device=cuda).manual_seed(H * C + Co)
+    x = (torch.randn(N, H, W, C, device=cuda, generator=g) * 0.5).bfloat16()
+    w = (torch.randn(Co, 3, 3, C, device=cuda, generator=g) * 0.05).bfloat16()
+    bias = torch.randn(Co, device=cuda, generator=g)
+    y = linear(x.reshape(-1, C), w.reshape(Co, 9 * C), bias=bias, conv=(N, Ho, Wo, C, 2), out_dtype=torch.float32,
+               bn=bn, split=split, pair=pair)
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), bias,
+                                     stride=2, padding=1)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Co)
+    err = (y - ref).abs().max().item()
+    assert err <= 2e-3 * max(1.0, ref.abs().max().item()), err

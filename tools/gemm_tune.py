@@ -73,8 +73,9 @@ def tune_shape(desc, dev, reps, cold=False):
     from paper_2603_25872_b200.netops import linear, pick
     M, N, K, act, res_f32, has_res, out_f32, conv = desc
     if conv is not None:
-        cn, ch, cw, cc = conv
-        x = torch.randn(cn * ch * cw, cc, device=dev).bfloat16()
+        cn, ch, cw, cc = conv[:4]
+        s2 = conv[4] if len(conv) > 4 else 1              # stride-2 conv: input is (s H) x (s W)
+        x = torch.randn(cn * ch * cw * s2 * s2, cc, device=dev).bfloat16()
     else:
         x = torch.randn(M, K, device=dev).bfloat16()
     w = (torch.randn(N, K, device=dev) * 0.02).bfloat16()
@@ -131,7 +132,7 @@ def main():
     for spec in a.nets:
         name, bs = spec.split(":")
         for d in collect(name, [int(b) for b in bs.split(",")], dev):
-            key = netops.table_key(d[0], d[1], d[2], d[7] is not None)
+            key = netops.table_key(d[0], d[1], d[2], False if d[7] is None else (d[7][4] if len(d[7]) > 4 else 1))
             if d[3] == "headsoftmax":          # fixed tile (bn 192, 1-SM): nothing to tune
                 continue
             if not a.mmax or d[0] <= a.mmax:

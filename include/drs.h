@@ -59,6 +59,9 @@ typedef struct drs_key {
  * denoiser.py:139-145 state_independent_eps.  One CTA per stream. */
 int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const uint64_t* seeds,
                    int64_t n, double* out, int64_t ld, int* err, void* stream);
+/* Measurement switch: 1 (default) = parallel chain resolve (slow-attempt list),
+ * 0 = the serial one-warp resolve.  Same output bits either way. */
+int drs_set_noise_resolve(int mode);
 
 /* ---- skip transitions (K2/K3) -------------------------------------------- */
 #define DRS_FAMILY_DDIM 0     /* ddim_skip                                   */

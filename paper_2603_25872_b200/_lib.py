@@ -122,6 +122,7 @@ _SIGS = {
     "drs_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_early_weights": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_chain_vec": (ctypes.c_int, [ctypes.c_int]),
+    "drs_set_noise_resolve": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_gn_mode": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_attn_split": (ctypes.c_int, [ctypes.c_int]),
     # include/drs_net.h

@@ -32,6 +32,10 @@
 
 namespace drs {
 
+// 0: serial one-warp resolve; 1 (default): parallel resolve over the slow list
+__device__ int g_resolve_mode = 1;
+__device__ __forceinline__ int resolve_mode() { return g_resolve_mode; }
+
 __device__ const uint64_t kZigKi[256] = DRS_ZIG_KI;
 __device__ const double kZigWi[256] = DRS_ZIG_WI;
 __device__ const double kZigFi[256] = DRS_ZIG_FI;
@@ -124,6 +128,128 @@ __device__ __forceinline__ void resolve(const double* __restrict__ vals, const u
   }
 }
 
+// ---- parallel resolve (all worker threads) ---------------------------------
+// The visit chain only branches at SLOW attempts (step > 1: wedge tests and
+// tails, ~1.5 % of positions): a position is visited iff it is >= the entry
+// cover and not strictly inside the span [s, s + step_s) of a VISITED slow
+// attempt s, and a slow attempt is visited iff it is not inside an earlier
+// visited span.  So: (1) the tile's slow positions are listed in order
+// (per-window ballots + a window prefix), (2) one thread walks only that short
+// list, (3) every worker marks the visited spans in a bitmap and (4) writes the
+// accepted values of visited positions at their prefix-sum output index.  Same
+// chain as `resolve` (bit-identical output), without 70 serial windows.
+template <int W>
+struct ResolveScratch {
+  static constexpr int kWin = W / 32;
+  uint16_t slow[W];             // slow positions, in order
+  int win_cnt[kWin];            // slow count, then accepted count, per window
+  int win_off[kWin];
+  uint32_t covered[kWin];       // bit p%32 of word p/32: inside a visited slow span
+  int n_slow;
+  int cover_out;
+  int64_t count_out;
+};
+
+__device__ __forceinline__ void wsync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
+
+// Exclusive prefix over kWin window counts (kWin <= 96), done by warp 0 of the workers.
+template <int kWin>
+__device__ __forceinline__ void window_scan(const int* cnt, int* off, int lane, int& total) {
+  int carry = 0;
+#pragma unroll
+  for (int b = 0; b < kWin; b += 32) {
+    const int v = b + lane < kWin ? cnt[b + lane] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b + lane < kWin) off[b + lane] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  total = carry;
+}
+
+template <int W>
+__device__ __forceinline__ void resolve_parallel(const double* __restrict__ vals, const uint8_t* __restrict__ steps,
+                                                 ResolveScratch<W>& sc, double* __restrict__ o, int64_t n,
+                                                 int64_t& count, int& cover, int tid, int nthreads, int bar_id) {
+  constexpr int kWin = W / 32;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthreads >> 5;
+  // (1) slow positions per window
+  for (int w = warp; w < kWin; w += nwarps) {
+    const unsigned slow = __ballot_sync(0xffffffffu, (steps[w * 32 + lane] & 0x7f) != 1);
+    if (lane == 0) { sc.win_cnt[w] = __popc(slow); sc.covered[w] = 0u; }
+  }
+  wsync(bar_id, nthreads);
+  if (warp == 0) {
+    int total;
+    window_scan<kWin>(sc.win_cnt, sc.win_off, lane, total);
+    if (lane == 0) sc.n_slow = total;
+  }
+  wsync(bar_id, nthreads);
+  for (int w = warp; w < kWin; w += nwarps) {
+    const bool sl = (steps[w * 32 + lane] & 0x7f) != 1;
+    const unsigned slow = __ballot_sync(0xffffffffu, sl);
+    if (sl) sc.slow[sc.win_off[w] + __popc(slow & ((1u << lane) - 1u))] = (uint16_t)(w * 32 + lane);
+  }
+  wsync(bar_id, nthreads);
+  // (2) walk the slow attempts in order (one thread; ~35 per 2240 positions);
+  //     a visited one is flagged by setting bit 15 of its list entry
+  if (tid == 0) {
+    int cov = cover;                              // first position not covered
+    const int ns = sc.n_slow;
+    for (int i = 0; i < ns; ++i) {
+      const int sp = sc.slow[i];
+      if (sp >= cov) {
+        cov = sp + (steps[sp] & 0x7f);
+        sc.slow[i] = (uint16_t)(sp | 0x8000);
+      }
+    }
+    sc.cover_out = cov > W ? cov - W : 0;
+  }
+  wsync(bar_id, nthreads);
+  // (3) mark the interiors of visited spans (and the entry cover) as covered
+  for (int i = tid; i < sc.n_slow; i += nthreads) {
+    const int e = sc.slow[i];
+    if (e & 0x8000) {
+      const int sp = e & 0x7fff;
+      const int end = min(W, sp + (steps[sp] & 0x7f));
+      for (int q = sp + 1; q < end; ++q) atomicOr(&sc.covered[q >> 5], 1u << (q & 31));
+    }
+  }
+  for (int q = tid; q < min(cover, W); q += nthreads) atomicOr(&sc.covered[q >> 5], 1u << (q & 31));
+  wsync(bar_id, nthreads);
+  // (4) accepted & visited -> output index (window prefix), coalesced stores
+  for (int w = warp; w < kWin; w += nwarps) {
+    const bool vis = !((sc.covered[w] >> lane) & 1u);
+    const bool acc = vis && ((steps[w * 32 + lane] >> 7) & 1);
+    const unsigned am = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) sc.win_cnt[w] = __popc(am);
+  }
+  wsync(bar_id, nthreads);
+  if (warp == 0) {
+    int total;
+    window_scan<kWin>(sc.win_cnt, sc.win_off, lane, total);
+    if (lane == 0) sc.count_out = count + total;
+  }
+  wsync(bar_id, nthreads);
+  for (int w = warp; w < kWin; w += nwarps) {
+    const bool vis = !((sc.covered[w] >> lane) & 1u);
+    const bool acc = vis && ((steps[w * 32 + lane] >> 7) & 1);
+    const unsigned am = __ballot_sync(0xffffffffu, acc);
+    if (acc) {
+      const int64_t oi = count + sc.win_off[w] + __popc(am & ((1u << lane) - 1u));
+      if (oi < n) o[oi] = vals[w * 32 + lane];
+    }
+  }
+  count = sc.count_out;
+  cover = sc.cover_out;
+}
+
 __device__ __forceinline__ void load_key(const drs_key* keys, const uint64_t* seeds, int sidx,
                                          uint32_t* ent, int& ne) {
   const drs_key k = keys[sidx];
@@ -143,6 +269,7 @@ noise_pcg64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict_
   __shared__ uint8_t steps[kW];               // bit7 = accept, bits0..6 = words consumed
   __shared__ u128 s_state, s_inc;
   __shared__ int64_t s_count;
+  __shared__ ResolveScratch<kW> sc;
   const int tid = threadIdx.x, lane = tid & 31;
   double* const o = out + (int64_t)blockIdx.x * ld;
   if (tid == 0) {
@@ -175,9 +302,14 @@ noise_pcg64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict_
     __syncthreads();
     classify(words, kWords, vals, steps, kW, tid, kThreads, local_err);
     __syncthreads();
-    if (tid < 32) {
-      resolve(vals, steps, kW, o, n, count, cover, lane);
-      if (lane == 0) s_count = count;
+    if (resolve_mode() == 0) {
+      if (tid < 32) {
+        resolve(vals, steps, kW, o, n, count, cover, lane);
+        if (lane == 0) s_count = count;
+      }
+    } else {
+      resolve_parallel<kW>(vals, steps, sc, o, n, count, cover, tid, kThreads, 0);
+      if (tid == 0) s_count = count;
     }
     __syncthreads();
     if (s_count >= n) break;
@@ -203,6 +335,7 @@ noise_sfc64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict_
   __shared__ double vals[kSfcW];
   __shared__ uint8_t steps[kSfcW];
   __shared__ int64_t s_count;
+  __shared__ ResolveScratch<kSfcW> sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* const o = out + (int64_t)blockIdx.x * ld;
   const bool gen_lane = warp == kSfcGenWarp && lane == 0;
@@ -237,9 +370,14 @@ noise_sfc64_kernel(const drs_key* __restrict__ keys, const uint64_t* __restrict_
     } else {
       classify(words[cur], kSfcWords, vals, steps, kSfcW, tid, kSfcWorkers, local_err);
       asm volatile("bar.sync 1, %0;" :: "n"(kSfcWorkers));
-      if (warp == 0) {
-        resolve(vals, steps, kSfcW, o, n, count, cover, lane);
-        if (lane == 0) s_count = count;
+      if (resolve_mode() == 0) {
+        if (warp == 0) {
+          resolve(vals, steps, kSfcW, o, n, count, cover, lane);
+          if (lane == 0) s_count = count;
+        }
+      } else {
+        resolve_parallel<kSfcW>(vals, steps, sc, o, n, count, cover, tid, kSfcWorkers, 1);
+        if (tid == 0) s_count = count;
       }
     }
     __syncthreads();
@@ -263,4 +401,9 @@ extern "C" int drs_noise_fill(int gen, const drs_key* keys, int n_streams, const
   else
     return DRS_ERR_VALUE;
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
+}
+
+extern "C" int drs_set_noise_resolve(int mode) {
+  if (mode < 0 || mode > 1) return DRS_ERR_VALUE;
+  return cudaMemcpyToSymbol(drs::g_resolve_mode, &mode, sizeof(int)) == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }

@@ -33,8 +33,18 @@ def _np_stream(key, n, gen):
     return np.random.Generator(np.random.SFC64(np.random.SeedSequence(key))).standard_normal(n)
 
 
+@pytest.fixture(params=[1, 0], ids=["parallel_resolve", "serial_resolve"])
+def resolve_mode(request, cuda):
+    """Both chain resolvers of K1 (drs_set_noise_resolve): they must give the same bits."""
+    from paper_2603_25872_b200 import _lib
+    _lib.check(_lib.lib().drs_set_noise_resolve(request.param), "drs_set_noise_resolve")
+    yield request.param
+    _lib.check(_lib.lib().drs_set_noise_resolve(1), "drs_set_noise_resolve")
+
+
 @pytest.mark.parametrize("gen", ["pcg64", "sfc64"])
-def test_golden_streams_bit_exact(cuda, golden_dir, gen):
+def test_golden_streams_bit_exact(cuda, golden_dir, gen, resolve_mode):
+    """Golden streams cover every ziggurat path: fast, wedge accept / reject, tail, tail retry."""
     for key, n, ref in _gold_streams(golden_dir, gen):
         got = _fill([key], n, gen, cuda)[0]
         assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (key, np.flatnonzero(got != ref)[:5])
@@ -42,7 +52,7 @@ def test_golden_streams_bit_exact(cuda, golden_dir, gen):
 
 @pytest.mark.parametrize("gen", ["pcg64", "sfc64"])
 @pytest.mark.parametrize("n", [1, 31, 2239, 2240, 2241, 4096, 16384, 65536])
-def test_random_keys_vs_numpy(cuda, gen, n):
+def test_random_keys_vs_numpy(cuda, gen, n, resolve_mode):
     rng = np.random.default_rng(n)
     keys = [(0x7A9C, int(rng.integers(0, 2 ** 48)), int(rng.integers(0, 300)), int(rng.integers(0, 3)))
             for _ in range(8 if n > 10000 else 24)]

@@ -17,6 +17,7 @@ LN GEGLU FF] -> proj_out + residual), Downsample2D (conv3x3 stride 2),
 Upsample2D (nearest 2x + conv3x3).
 """
 
+import contextlib
 import os
 from dataclasses import dataclass, field
 
@@ -87,6 +88,9 @@ class UNet:
         self.fused_qkv = os.environ.get("DRS_QKV_FUSED", "1") != "0"
         # stride-2 downsampling convs as implicit GEMMs (DRS_STRIDED_CONV=0: im2col + GEMM)
         self.strided_conv = os.environ.get("DRS_STRIDED_CONV", "1") != "0"
+        # resblock 1x1 shortcuts on a side stream (DRS_SIDE_SHORTCUT=0: in line)
+        side = os.environ.get("DRS_SIDE_SHORTCUT", "1") != "0" and self.device.type == "cuda"
+        self._side = torch.cuda.Stream(self.device) if side else None
         I = _Init(self.device, seed)
         c0, T = cfg.channels[0], cfg.temb_dim
         self.p = p = {}
@@ -262,6 +266,22 @@ class UNet:
             ops.im2col(x, c1, skip, c2, N, H, W, 1, 1, 0, 1, cat)
             x = cat
         cin = c1 + c2
+        ev = None
+        if r["sc"] is not None:
+            short = self.buf(f"sc{co}_{HW}", (N * HW, co))
+            if self._side is not None:
+                # the 1x1 shortcut only needs x: it runs on a side stream (a parallel
+                # branch of the captured graph) under GN1 -> conv1 -> GN2
+                main = torch.cuda.current_stream(self.device)
+                self._side.wait_stream(main)
+                with torch.cuda.stream(self._side):
+                    self._lin(x, r["sc"][0], bias=r["sc"][1], out=short)
+                    ev = torch.cuda.Event()
+                    ev.record(self._side)
+            else:
+                self._lin(x, r["sc"][0], bias=r["sc"][1], out=short)
+        else:
+            short = x
         hn = self.buf(f"gn{cin}_{HW}", (N * HW, cin))
         ops.groupnorm(x, N, HW, cin, self.cfg.groups, r["gn1"][0], r["gn1"][1], hn, eps=1e-5, silu=True)
         h1 = self.buf(f"r1_{co}_{HW}", (N * HW, co))
@@ -269,11 +289,8 @@ class UNet:
         self._conv3(hn, cin, None, 0, N, H, W, r["conv1"], out=h1, rowbias=tb, rb_group=HW * self._tg)
         hn2 = self.buf(f"gn{co}_{HW}", (N * HW, co))
         ops.groupnorm(h1, N, HW, co, self.cfg.groups, r["gn2"][0], r["gn2"][1], hn2, eps=1e-5, silu=True)
-        if r["sc"] is not None:
-            short = self.buf(f"sc{co}_{HW}", (N * HW, co))
-            self._lin(x, r["sc"][0], bias=r["sc"][1], out=short)
-        else:
-            short = x
+        if ev is not None:
+            torch.cuda.current_stream(self.device).wait_event(ev)
         out = self.buf(out_tag or f"res_out{co}_{HW}", (N * HW, co))
         self._conv3(hn2, co, None, 0, N, H, W, r["conv2"], out=out, residual=short)
         return out
@@ -345,42 +362,54 @@ class UNet:
         for b, x in enumerate(xs):
             ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b) * HW:(2 * b + 1) * HW])
             ops.latent_to_nhwc(x, cfg.in_ch, HW, 64, x_in[(2 * b + 1) * HW:(2 * b + 2) * HW])
-        if cfg.add_embed_dim:
-            # SDXL: the added (pooled text + size) embedding differs between the CFG
-            # images, so the time embedding is per image (N rows)
-            tpair = self.buf("tpair", (N,), torch.float32)
-            tpair.view(B, 2).copy_(t_dev[:B, None].expand(B, 2))
-            tf = self.buf("tfreq", (N, cfg.channels[0]))
-            ops.timestep_embedding(tpair, cfg.channels[0], tf)
-            th = self.buf("th", (N, cfg.temb_dim))
-            self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
-            temb = self.buf("temb", (N, cfg.temb_dim), torch.float32)
-            ah = self.buf("ah", (N, cfg.temb_dim))
-            self._lin(self.add_in_rep[:N], p["a1"][0], bias=p["a1"][1], act="silu", out=ah)
-            aemb = self.buf("aemb", (N, cfg.temb_dim), torch.float32)
-            self._lin(ah, p["a2"][0], bias=p["a2"][1], out=aemb)
-            self._lin(th, p["t2"][0], bias=p["t2"][1], residual=aemb, out=temb)
-            temb_act = self.buf("temb_act", (N, cfg.temb_dim))
-            ops.silu_cast(temb, temb_act)
-            self._tg = 1                                  # temb rows per image
-            n_t = N
-        else:
-            # SD1.5: both CFG images share the timestep, so the embedding MLP runs once
-            # per pair (B rows), SiLU fused into the second linear's epilogue, and the
-            # resblocks index the per-pair row (row bias group = 2 HW)
-            tf = self.buf("tfreq", (B, cfg.channels[0]))
-            ops.timestep_embedding(t_dev[:B], cfg.channels[0], tf)
-            th = self.buf("th", (B, cfg.temb_dim))
-            self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
-            temb_act = self.buf("temb_act", (B, cfg.temb_dim))
-            self._lin(th, p["t2"][0], bias=p["t2"][1], act="silu", out=temb_act)
-            self._tg = 2
-            n_t = B
-        temb_all = self.buf("temb_all", (n_t, self.temb_w.shape[0]), torch.float32)
-        self._lin(temb_act, self.temb_w, bias=self.temb_b, out=temb_all)
+        # the time-embedding MLP (M <= 2B rows: GEMVs) only needs t: a side-stream branch
+        # of the captured graph, in parallel with the input layout + conv_in
+        main = torch.cuda.current_stream(self.device)
+        temb_ev = None
+        if self._side is not None:
+            self._side.wait_stream(main)
+        with torch.cuda.stream(self._side) if self._side is not None else contextlib.nullcontext():
+            if cfg.add_embed_dim:
+                # SDXL: the added (pooled text + size) embedding differs between the CFG
+                # images, so the time embedding is per image (N rows)
+                tpair = self.buf("tpair", (N,), torch.float32)
+                tpair.view(B, 2).copy_(t_dev[:B, None].expand(B, 2))
+                tf = self.buf("tfreq", (N, cfg.channels[0]))
+                ops.timestep_embedding(tpair, cfg.channels[0], tf)
+                th = self.buf("th", (N, cfg.temb_dim))
+                self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
+                temb = self.buf("temb", (N, cfg.temb_dim), torch.float32)
+                ah = self.buf("ah", (N, cfg.temb_dim))
+                self._lin(self.add_in_rep[:N], p["a1"][0], bias=p["a1"][1], act="silu", out=ah)
+                aemb = self.buf("aemb", (N, cfg.temb_dim), torch.float32)
+                self._lin(ah, p["a2"][0], bias=p["a2"][1], out=aemb)
+                self._lin(th, p["t2"][0], bias=p["t2"][1], residual=aemb, out=temb)
+                temb_act = self.buf("temb_act", (N, cfg.temb_dim))
+                ops.silu_cast(temb, temb_act)
+                self._tg = 1                                  # temb rows per image
+                n_t = N
+            else:
+                # SD1.5: both CFG images share the timestep, so the embedding MLP runs once
+                # per pair (B rows), SiLU fused into the second linear's epilogue, and the
+                # resblocks index the per-pair row (row bias group = 2 HW)
+                tf = self.buf("tfreq", (B, cfg.channels[0]))
+                ops.timestep_embedding(t_dev[:B], cfg.channels[0], tf)
+                th = self.buf("th", (B, cfg.temb_dim))
+                self._lin(tf, p["t1"][0], bias=p["t1"][1], act="silu", out=th)
+                temb_act = self.buf("temb_act", (B, cfg.temb_dim))
+                self._lin(th, p["t2"][0], bias=p["t2"][1], act="silu", out=temb_act)
+                self._tg = 2
+                n_t = B
+            temb_all = self.buf("temb_all", (n_t, self.temb_w.shape[0]), torch.float32)
+            self._lin(temb_act, self.temb_w, bias=self.temb_b, out=temb_all)
+            if self._side is not None:
+                temb_ev = torch.cuda.Event()
+                temb_ev.record(self._side)
 
         h = self.buf("h_in", (N * HW, cfg.channels[0]))
         self._conv3(x_in, 64, None, 0, N, S, S, p["conv_in"], out=h)
+        if temb_ev is not None:
+            main.wait_event(temb_ev)
         H = W = S
         cur_c = cfg.channels[0]
         saved = [(h, H)]                  # h_in is written once per forward: no copy
@@ -411,6 +440,8 @@ class UNet:
         ops.groupnorm(h, N, HW, cur_c, cfg.groups, p["gn_out"][0], p["gn_out"][1], hn, eps=1e-5, silu=True)
         y = self.buf("y_out", (N * HW, cfg.out_ch), torch.float32)
         self._conv3(hn, cur_c, None, 0, N, S, S, p["conv_out"], out=y)
+        if self._side is not None:              # join the side stream (graph capture needs it)
+            torch.cuda.current_stream(self.device).wait_stream(self._side)
         for b in range(B):
             dst = outs[b] if outs is not None else self.buf(f"eps{b}", (self.latent_numel,), torch.float32)
             ops.cfg_combine(y[2 * b * HW:(2 * b + 2) * HW], HW, cfg.in_ch, self.cfg_scale, True, dst)

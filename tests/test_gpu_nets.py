@@ -183,6 +183,8 @@ def test_attention_tc_kernel(cuda, B, H, Lq, Lk, d, amp):
 
 
 @pytest.mark.parametrize("N,HW,C,G,f32,silu", [(2, 4096, 320, 32, False, True), (2, 1024, 640, 32, True, False),
+                                               (2, 1024, 1920, 32, False, True), (2, 256, 2560, 32, False, True),
+                                               (2, 4096, 960, 32, False, False), (1, 16384, 640, 32, False, True),
                                                (2, 64, 1280, 32, False, True), (16, 4096, 320, 32, False, True),
                                                (2, 16384, 320, 32, False, False), (3, 100, 960, 32, False, True),
                                                (2, 256, 64, 32, False, True)])

@@ -480,13 +480,22 @@ class DeviceRun:
         torch.cuda.current_stream(self.device).wait_stream(s)
         torch.cuda.synchronize(self.device)
         if not self.gather_rounds or self.comm.capturable:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
-                self.enqueue()
-            self.graph, self.seg_graphs = g, None
-            self.graph_mode = "one graph" + (" (NCCL all-gathers captured)" if self.gather_rounds else "")
-            return g
-        self.graph_mode = "per-segment graphs, host-staged exchange between replays"
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.enqueue()
+                self.graph, self.seg_graphs = g, None
+                self.graph_mode = "one graph" + (" (NCCL all-gathers captured)" if self.gather_rounds else "")
+                return g
+            except RuntimeError as exc:
+                if not self.gather_rounds:
+                    raise
+                # a collective that refuses capture: per-segment graphs with the same
+                # all-gathers issued between replays (NCCL matches collectives by order,
+                # so ranks that captured and ranks that did not stay in step)
+                torch.cuda.synchronize(self.device)
+                self.capture_error = str(exc)
+        self.graph_mode = "per-segment graphs, exchange between replays"
         self.seg_graphs = []
         for i in range(len(self.segments)):
             g = torch.cuda.CUDAGraph()

@@ -31,10 +31,13 @@ def main():
         n_t = -(-N // bn)
         m_t = -(-M // (256 if pr else 128))
         traffic = (M * K * 2) * n_t + (N * K * 2) * m_t
-        rows.append((t, bn, sp, pr, traffic / 1e6))
-    for t, bn, sp, pr, mb in sorted(rows):
-        print(f"{M}x{N}x{K} bn={bn:3d} split={sp} pair={pr}: {t:7.2f} us  L2 operand traffic {mb:7.1f} MB "
-              f"({mb / 1e3 / (t * 1e-6) / 1e3 if t else 0:5.2f} TB/s)")
+        ctas = (m_t * n_t * (2 if pr else 1)) * sp
+        kb = -(-K // 64) / sp
+        per_cta = kb * (128 * 128 + (bn // 2 if pr else bn) * 128)      # A 128 rows + (half) B tile per k-block
+        rows.append((t, bn, sp, pr, traffic / 1e6, ctas, per_cta / 1e3))
+    for t, bn, sp, pr, mb, ctas, pc in sorted(rows):
+        print(f"{M}x{N}x{K} bn={bn:3d} split={sp} pair={pr}: {t:7.2f} us  L2 traffic {mb:6.1f} MB  {ctas:4d} CTAs "
+              f"x {pc:6.0f} KB/CTA ({pc / t:5.1f} KB/us/CTA)")
 
 
 if __name__ == "__main__":

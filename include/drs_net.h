@@ -127,8 +127,12 @@ int drs_gemv(const void* x, int64_t ldx, const void* w, int64_t ldw, const float
              int64_t ldr, int res_f32, void* out, int64_t ldo, int out_f32, int M, int N, int K, int act,
              int ctas_per_sm /* 0: 4 per SM; 1: leaves room for co-resident GEMM CTAs */, void* stream);
 
-/* Measurement switch: 1 (default) = attention with separate S and PV MMA issuer warps, 0 = one. */
+/* Measurement switch: 0 = attention with one MMA warp, 1 = separate S and PV MMA issuer warps,
+ * 2 (default) = 1 + the softmax on the paired FP32 pipe, 3 = 2 + two P buffers per softmax set (d <= 64). */
 int drs_set_attn_split(int on);
+/* Measurement switch: 1 = the (query tile, head, image) items of the last partial wave of an
+ * attention launch run as two key-range halves (combined by the second to finish); 0 (default). */
+int drs_set_attn_tail_split(int on);
 
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);

@@ -275,6 +275,46 @@ def test_sd15_cross_attention_fold_batched(cuda, size, B, g):
             assert rel < 3e-2, (fold, b, rel)
 
 
+@pytest.mark.parametrize("B,H,Lq,Lk,d,amp", [(2, 8, 4096, 4096, 40, 1), (1, 5, 300, 2500, 64, 6),
+                                             (3, 7, 130, 2049, 40, 6), (2, 10, 4096, 4096, 64, 1),
+                                             (1, 3, 1000, 1500, 32, 6), (2, 8, 1024, 1024, 80, 1)])
+@pytest.mark.parametrize("mode,tail", [(0, 0), (1, 0), (2, 0), (3, 0), (2, 1), (3, 1)])
+def test_attention_modes(cuda, B, H, Lq, Lk, d, amp, mode, tail):
+    """Every attention variant vs torch fp32: one / two MMA issuer warps, the
+    paired-FP32 softmax, two P buffers per set, and the tail split (items of the
+    last partial wave run as two key halves, combined by the second to finish --
+    the first four shapes trigger it, incl. an odd number of key tiles and a
+    ragged last tile). Repeats are bit-identical (the combine is written in half
+    order, whichever half runs it)."""
+    from paper_2603_25872_b200 import _lib
+    from paper_2603_25872_b200.netops import attention_qkv
+    L = _lib.lib()
+    L.drs_set_attn_split(mode)
+    L.drs_set_attn_tail_split(tail)
+    try:
+        g = torch.Generator(device=cuda).manual_seed(Lq + Lk + d)
+        q = (amp * torch.randn(B * Lq, H * d, device=cuda, generator=g)).bfloat16()
+        kv = torch.randn(B * Lk, 2 * H * d, device=cuda, generator=g).bfloat16()
+        k, v = kv[:, :H * d], kv[:, H * d:]
+        full = torch.full((B * Lq + 130, H * d), 7.0, device=cuda, dtype=torch.bfloat16)
+        out = full[:B * Lq]
+        attention_qkv(q, k, v, out, B, H, Lq, Lk, d)
+        first = out.clone()
+        for _ in range(3):
+            attention_qkv(q, k, v, out, B, H, Lq, Lk, d)
+            assert torch.equal(out, first)
+        Q = q.float().reshape(B, Lq, H, d).transpose(1, 2)
+        K = k.float().reshape(B, Lk, H, d).transpose(1, 2)
+        V = v.float().reshape(B, Lk, H, d).transpose(1, 2)
+        ref = (torch.softmax(Q @ K.transpose(-1, -2) / math.sqrt(d), -1) @ V).transpose(1, 2).reshape(B * Lq, H * d)
+        rel = ((out.float() - ref).norm() / ref.norm()).item()
+        assert rel < 1e-2, rel
+        assert bool((full[B * Lq:] == 7.0).all())
+    finally:
+        L.drs_set_attn_split(2)
+        L.drs_set_attn_tail_split(0)
+
+
 @pytest.mark.parametrize("B,H,Lq,Lk,d,amp", [(2, 8, 1024, 1024, 40, 1), (1, 16, 256, 256, 72, 1),
                                              (2, 10, 256, 256, 64, 1), (1, 5, 300, 333, 64, 6),
                                              (3, 4, 70, 300, 160, 1), (2, 2, 129, 77, 96, 6),

@@ -31,14 +31,20 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--only", default="", help="substring of the shape label to run")
     ap.add_argument("--eager", type=int, default=0, help="N eager launches only (for ncu), no timing")
-    ap.add_argument("--split", type=int, default=1, help="separate S / PV MMA issuer warps (1) or one (0)")
+    ap.add_argument("--split", type=int, default=2, help="attention variant (drs_set_attn_split)")
+    ap.add_argument("--tail", type=int, default=0, help="split the last partial wave over key halves (1) or not")
+    ap.add_argument("--shapes", default="", help="custom shapes 'B,H,Lq,Lk,d;...' instead of the UNet/DiT list")
     a = ap.parse_args()
+    shapes = SHAPES
+    if a.shapes:
+        shapes = [("custom",) + tuple(int(v) for v in t.split(",")) for t in a.shapes.split(";") if t]
     import torch
     from paper_2603_25872_b200 import _lib, netops
     _lib.lib().drs_set_attn_split(a.split)
+    _lib.lib().drs_set_attn_tail_split(a.tail)
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
-    for label, B, H, Lq, Lk, d in SHAPES:
+    for label, B, H, Lq, Lk, d in shapes:
         if a.only and a.only not in label:
             continue
         vt_img = (Lk + 7) // 8 * 8

@@ -18,11 +18,15 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--early", type=int, default=1, help="GEMM weight tiles requested before the PDL wait")
+    ap.add_argument("--attn", type=int, default=2, help="attention variant (drs_set_attn_split)")
+    ap.add_argument("--tail", type=int, default=0, help="attention tail split (drs_set_attn_tail_split)")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import _lib
     _lib.lib().drs_set_pdl(a.pdl)
     _lib.lib().drs_set_early_weights(a.early)
+    _lib.lib().drs_set_attn_split(a.attn)
+    _lib.lib().drs_set_attn_tail_split(a.tail)
     dev = torch.device("cuda", 0)
     if a.net == "dit":
         from paper_2603_25872_b200.dit import DiT, DiTConfig

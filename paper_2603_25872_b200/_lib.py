@@ -17,6 +17,7 @@ DRS_OK = 0
 GEN_PCG64 = 0
 GEN_SFC64 = 1
 FAMILY_DDIM = 0
+GEMM_KB2_DEFAULT = 0          # drs_set_gemm_kb2 default (csrc/gemm_tc.cu gemm_kb2_mode)
 FAMILY_DDPM = 1
 FAMILY_DDPM_X0 = 2
 FAMILY_PRED_X0 = 3
@@ -78,7 +79,7 @@ class DrsGemmArgs(ctypes.Structure):       # include/drs_net.h drs_gemm_args
         ("cta_pair", ctypes.c_int),
         ("b_img_rows", ctypes.c_int), ("b_img_off", ctypes.c_int), ("hs_valid", ctypes.c_int),
         ("out2", ctypes.c_void_p), ("ldo2", ctypes.c_int64),
-        ("conv_stride", ctypes.c_int),
+        ("conv_stride", ctypes.c_int), ("kbox", ctypes.c_int),
     ]
 
 
@@ -121,6 +122,7 @@ _SIGS = {
     "drs_version": (ctypes.c_int, []),
     "drs_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_early_weights": (ctypes.c_int, [ctypes.c_int]),
+    "drs_set_gemm_kb2": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_chain_vec": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_noise_resolve": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_gn_mode": (ctypes.c_int, [ctypes.c_int]),

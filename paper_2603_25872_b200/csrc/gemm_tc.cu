@@ -145,6 +145,8 @@ struct EpiParams {
   void* out2;               // kEpi 4: a bf16 copy of the (fp32) output, row stride ldo2
   int64_t ldo2;
   int early_b;              // 1: weight tiles of the first stages requested before the PDL wait
+  int kb2;                  // 1: A / B tensor maps are 3-D [K/64][rows][64] views and one TMA box
+                            //    carries 2 k-blocks (2 ring stages: one full/empty barrier pair)
 };
 
 // kEpi 4: the finished row segment (32 values) also goes to the bf16 copy
@@ -450,6 +452,12 @@ __device__ __forceinline__ int b_row_offset(const ConvGeom& cv, int m0) {
   return cv.b_img_rows > 0 ? ((m0 / cv.b_img_rows) & 1) * cv.b_img_off : 0;
 }
 
+__device__ __forceinline__ void tma_load_3d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                            int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3) {
   asm volatile(
@@ -515,11 +523,16 @@ struct OutMaps {
   CUtensorMap r;
 };        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
 
+// The ring keeps the A tiles of all stages together, then the B tiles, so the
+// tiles of stages s and s+1 are adjacent and one 2-k-block TMA box (kb2 mode)
+// fills both.
 template <int BN, int kStages>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kAOff = 0;                              // A tile of stage s: kAOff + s * kABytes
+  static constexpr int kBOff = kStages * kABytes;              // B tile of stage s: kBOff + s * kBBytes
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
   static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;   // barriers; +1024 alignment slack
@@ -579,16 +592,23 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       // B tiles of the first kStages k-blocks are requested BEFORE the PDL wait,
       // so the cold weight stream overlaps the previous kernel's tail (the
       // stage's full barrier also expects the A bytes, which follow the wait).
+      // kb2: a ring slot ("super-stage") is 2 consecutive stages = 2 k-blocks,
+      // loaded by one 3-D box per operand (conv A: one 4-D box per k-block)
+      const int kpb = ep.kb2 ? 2 : 1;
+      const int nst = kStages / kpb;
       int pre = 0;
       if ((int)blockIdx.x < num_tiles) {
         const int sp = blockIdx.x % split, mn = blockIdx.x / split;
         const int mt = mn % m_tiles, nt = mn / m_tiles;
         const int kb0 = sp * kb_per_split, kb1 = min(num_kb_total, kb0 + kb_per_split);
-        pre = ep.early_b ? max(0, min(kStages, kb1 - kb0)) : 0;
+        pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
         for (int j = 0; j < pre; ++j) {
-          uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
-          tc::mbar_arrive_expect_tx(&full_bar[j], S::kStageBytes);
-          tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+          uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
+          tc::mbar_arrive_expect_tx(&full_bar[j], kpb * S::kStageBytes);
+          if (kpb == 2)
+            tma_load_3d(&tmap_b, &full_bar[j], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb0 + 2 * j);
+          else
+            tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
         }
       }
       pdl_wait();
@@ -600,29 +620,40 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
         const int mt = mn % m_tiles, nt = mn / m_tiles;
         const int kb0 = sp * kb_per_split;
         const int kb1 = min(num_kb_total, kb0 + kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          const bool b_done = tile == (int)blockIdx.x && kb - kb0 < pre;   // weights already in flight
+        for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
+          const bool b_done = tile == (int)blockIdx.x && j < pre;   // weights already in flight
           if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * S::kStageBytes;
-          uint8_t* sb = sa + S::kABytes;
-          if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
+          uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
+          if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], kpb * S::kStageBytes);
           if (cv.on) {
-            const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
-            const int ky = tap / 3, kx = tap - ky * 3;
-            const int m0 = mt * kBM, hw = cv.H * cv.W;
-            const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-            tma_load_4d(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
+            for (int q = 0; q < kpb; ++q) {       // a missing 2nd k-block of a conv: zero A bytes via the
+              const int k = min(kb + q, num_kb_total - 1);   // last valid box again (its MMA is skipped)
+              const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
+              const int ky = tap / 3, kx = tap - ky * 3;
+              const int m0 = mt * kBM, hw = cv.H * cv.W;
+              const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+              tma_load_4d(&tmap_a, &full_bar[stage], sa + q * S::kABytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
+            }
+          } else if (kpb == 2) {
+            tma_load_3d(&tmap_a, &full_bar[stage], sa, 0, mt * kBM, kb);
           } else {
             tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
           }
-          if (!b_done)
-            tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (!b_done) {
+            if (kpb == 2)
+              tma_load_3d(&tmap_b, &full_bar[stage], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb);
+            else
+              tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+          }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    const int kpb = ep.kb2 ? 2 : 1;
+    const int nst = kStages / kpb;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -635,21 +666,22 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; kb += kpb) {
         tc::mbar_wait(&full_bar[stage], phase);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          const uint8_t* sa = smem + stage * S::kStageBytes;
-          const uint64_t da = tc::smem_desc_sw128(sa);
-          const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+          for (int q = 0; q < kpb && kb + q < kb1; ++q) {
+            const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
+            const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)      // +32 B per K=16 step inside the swizzle atom
-            tc::mma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k)      // +32 B per K=16 step inside the swizzle atom
+              tc::mma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+          }
           tc::mma_commit(&empty_bar[stage]);
-          if (kb == kb1 - 1) tc::mma_commit(&tfull_bar[acc]);
+          if (kb + kpb >= kb1) tc::mma_commit(&tfull_bar[acc]);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == nst) { stage = 0; phase ^= 1; }
       }
       if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
         if (tc::elect_one()) tc::mma_commit(&tfull_bar[acc]);
@@ -1250,6 +1282,26 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
 // H, W: the OUTPUT grid; the input is (s H) x (s W).  With s = 2 the box spans
 // 2 W x 2 rows input elements traversed with element stride 2, i.e. it loads the
 // same 128 x 64-channel tile of pixels (s y + ky - 1, s x + kx - 1).
+// 3-D view [K/64][rows][64] of a K-contiguous bf16 matrix (K % 64 == 0): a
+// {64, box_rows, 2} box is two consecutive k-block tiles (kb2 mode)
+static bool make_tmap_kb2(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)rows, (cuuint64_t)(K / kBK)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(kBK * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// drs_set_gemm_kb2: 1-SM kernels load 2 k-blocks per TMA box when K % 64 == 0
+inline int& gemm_kb2_mode() {
+  static int on = 0;
+  return on;
+}
+
 static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
@@ -1577,8 +1629,13 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
       return DRS_ERR_VALUE;
     if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C, cs)) return DRS_ERR_CUDA;
     cv = ConvGeom{1, C / 64, H, W, 0, 0, cs};
-  } else if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) {
-    return DRS_ERR_CUDA;
+  }
+  // kb2 (1-SM kernels only, K % 64 == 0): one TMA box carries 2 k-blocks -- half the
+  // TMA operations, whose per-op issue cost (~190 clk from one thread) bounds the
+  // operand stream of small tiles (tools/micro/tma_kb2.cu)
+  const bool kb2_ok = (g->kbox == 2 || (g->kbox == 0 && gemm_kb2_mode())) && K % kBK == 0 && !hsm;
+  if (!g->conv_C) {
+    if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
   }
   if (g->b_img_rows > 0) {
     cv.b_img_rows = g->b_img_rows;
@@ -1586,7 +1643,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0, g->out2, g->ldo2,
-               early_weights_enabled()};
+               early_weights_enabled(), 0};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   OutMaps tcm;
   memset(&tcm, 0, sizeof(tcm));
@@ -1607,8 +1664,14 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   // split == 1 pair runs the persistent TMA epilogue only (decided here: the B map's box depends on it)
   const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM)) &&
                     (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
-  if (!make_tmap(&tb, g->B, N + (g->b_img_rows > 0 ? g->b_img_off : 0), K, g->ldb, pair ? bn / 2 : bn))
+  const int64_t b_rows = N + (g->b_img_rows > 0 ? g->b_img_off : 0);
+  if (kb2_ok && !pair) {
+    ep.kb2 = 1;
+    if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
+    if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, bn)) return DRS_ERR_CUDA;
+  } else if (!make_tmap(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn)) {
     return DRS_ERR_CUDA;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (g->out2) {                                   // plain epilogue + bf16 copy of the fp32 output
     if (g->act != DRS_ACT_NONE || g->rowbias || g->colscale || !g->out_f32 || (g->ldo2 % 8) ||
@@ -1633,4 +1696,9 @@ extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
   g.bias = bias; g.residual = residual; g.ldr = ldr; g.act = act; g.out_f32 = out_f32; g.alpha = alpha;
   g.bn = bn; g.split = split; g.workspace = workspace;
   return drs_gemm(&g, stream);
+}
+
+extern "C" int drs_set_gemm_kb2(int on) {
+  drs::gemm_kb2_mode() = on ? 1 : 0;
+  return DRS_OK;
 }

@@ -26,14 +26,15 @@ def _ptr(t):
 
 def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfloat16, alpha=1.0,
            bn=0, split=0, colscale=None, cs_group=0, rowbias=None, rb_group=0, conv=None, pair=None,
-           b_img=None, hs_valid=0, out2=None, gemv_ctas=0):
+           b_img=None, hs_valid=0, out2=None, gemv_ctas=0, kbox=0):
     """out[M, N'] = act(alpha * x[M, K] @ w[N, K]^T + bias + rowbias) * colscale (+ residual);
     N' = N/2 for geglu.  residual may be bf16 or fp32 (same shape as out); colscale /
     rowbias (n_groups, >=N) views indexed by row // group.  b_img = (rows, off): rows
     of images with odd index (row // rows) use w[off + n] instead of w[n] (w holds
     N + off rows; CFG pairs with per-context weights).  act="headsoftmax": per
     96-column head, softmax (exp2) over the first hs_valid columns.  out2: a bf16
-    tensor that also receives the (fp32) output, rounded."""
+    tensor that also receives the (fp32) output, rounded.  kbox: k-blocks per TMA box
+    (0: the tuned table / library default, 1, 2)."""
     assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
     if (conv is None and x.shape[0] <= 4 and act in (None, "none", "silu") and colscale is None and rowbias is None
             and b_img is None and out2 is None and GEMV and _gemv_ok(x, w)):
@@ -71,10 +72,14 @@ def linear(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.b
         SHAPES.append((M, N, K, act, residual is not None and residual.dtype == torch.float32,
                        residual is not None, out.dtype == torch.float32, None if conv is None else tuple(conv)))
     if bn == 0 or split == 0:                    # tuned table, else the library cost model
-        bn, split, tpair = pick3(M, N, K, bn, split, False if conv is None else (conv[4] if len(conv) > 4 else 1))
+        cv = False if conv is None else (conv[4] if len(conv) > 4 else 1)
+        bn, split, tpair = pick3(M, N, K, bn, split, cv)
         if pair is None:
             pair = tpair
+        if kbox == 0:
+            kbox = table_kbox(M, N, K, cv)
     g.bn, g.split = bn, split
+    g.kbox = kbox
     g.cta_pair = 1 if pair else 0
     if conv is not None:
         g.conv_N, g.conv_H, g.conv_W, g.conv_C = conv[:4]
@@ -128,7 +133,8 @@ def gemv(x, w, bias=None, act=None, residual=None, out=None, out_dtype=torch.bfl
 BN_CHOICES = (64, 128, 160, 192, 256)
 
 
-_TABLE_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gemm_table.json")
+_TABLE_PATH = os.environ.get("DRS_GEMM_TABLE") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                                "gemm_table.json")
 _TABLE = None
 SHAPES = None      # when a list: linear() appends (M, N, K, act, res_f32, has_res, out_f32, conv) (tuning)
 GEMM_RECORD = None  # when a list: linear() appends (flops, drs_gemm_args copy) -- bench.py replays them
@@ -161,6 +167,12 @@ def pick3(M, N, K, bn=0, split=0, conv=False):
             return (hit[0], hit[1], bool(hit[2]) if len(hit) > 2 else False)
     b, sp = pick(M, N, K, bn, split, conv)
     return b, sp, False
+
+
+def table_kbox(M, N, K, conv=False):
+    """k-blocks per TMA box the tuned table holds for this shape (0: library default)."""
+    hit = _table().get(table_key(M, N, K, conv))
+    return int(hit[3]) if hit is not None and len(hit) > 3 else 0
 
 
 def pick(M, N, K, bn=0, split=0, conv=False):

@@ -114,6 +114,39 @@ def tune_shape(desc, dev, reps, cold=False):
     return best, results[best], results, model
 
 
+def tune_kbox(desc, cfg, dev, reps, cold=False):
+    """Time the table's (bn, split) for this shape with 1 and 2 k-blocks per TMA box
+    (1-SM kernels; pair entries keep 1)."""
+    import torch
+    from paper_2603_25872_b200.netops import linear
+    M, N, K, act, res_f32, has_res, out_f32, conv = desc
+    if conv is not None:
+        cn, ch, cw, cc = conv[:4]
+        s2 = conv[4] if len(conv) > 4 else 1
+        x = torch.randn(cn * ch * cw * s2 * s2, cc, device=dev).bfloat16()
+    else:
+        x = torch.randn(M, K, device=dev).bfloat16()
+    w = (torch.randn(N, K, device=dev) * 0.02).bfloat16()
+    copies = max(1, min(reps, -(-(256 << 20) // (N * K * 2)))) if cold else 1
+    ws = [w] + [w.clone() for _ in range(copies - 1)]
+    wi = [0]
+
+    def wnext():
+        wi[0] = (wi[0] + 1) % copies
+        return ws[wi[0]]
+    n_out = N // 2 if act == "geglu" else N
+    out = torch.empty(M, n_out, device=dev, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    res = torch.randn(M, n_out, device=dev, dtype=torch.float32 if res_f32 else torch.bfloat16) if has_res else None
+    bias = torch.randn(N, device=dev)
+    bn, sp = cfg[0], cfg[1]
+    t = {}
+    for kbox in (1, 2):
+        run = lambda kbox=kbox: linear(x, wnext(), bias=bias, act=act, residual=res, out=out, bn=bn,   # noqa: E731
+                                       split=sp, conv=conv, pair=False, kbox=kbox)
+        t[kbox] = time_config(run, reps)
+    return t
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nets", nargs="+", default=["sd15:1,2,4,8", "dit:1,2,4,8", "sdxl:1,2"])
@@ -123,6 +156,8 @@ def main():
     ap.add_argument("--mmax", type=int, default=0, help="only shapes with M <= mmax")
     ap.add_argument("--merge", action="store_true", help="update the existing table instead of replacing it")
     ap.add_argument("--only-missing", action="store_true", help="with --merge: tune only shapes not in the table")
+    ap.add_argument("--kbox", action="store_true",
+                    help="keep each entry's (bn, split, pair); choose 1 or 2 k-blocks per TMA box for 1-SM entries")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import netops
@@ -143,6 +178,21 @@ def main():
     if a.merge and os.path.exists(base):
         table = {k: list(v) for k, v in json.load(open(base))["configs"].items()}
     tot_best = tot_model = 0.0
+    if a.kbox:
+        tot1 = tot_sel = 0.0
+        for key, d in sorted(uniq.items()):
+            cfg = table.get(key)
+            if cfg is None or (len(cfg) > 2 and cfg[2]) or d[2] % 64:
+                continue
+            t = tune_kbox(d, cfg[:2], dev, a.reps, a.cold)
+            kbox = 2 if t[2] < t[1] * 0.98 else 1
+            table[key] = list(cfg[:3]) + [kbox] if len(cfg) > 2 else list(cfg[:2]) + [0, kbox]
+            tot1 += t[1]
+            tot_sel += t[kbox]
+            print(f"{key:24s} bn={cfg[0]:3d} split={cfg[1]}  kbox1 {t[1]:8.1f} us  kbox2 {t[2]:8.1f} us -> {kbox}",
+                  flush=True)
+        print(f"kbox pass: sum {tot1:.0f} us (1 k-block per box) -> {tot_sel:.0f} us (selected)")
+        uniq = {}
     if a.only_missing:
         uniq = {k: d for k, d in uniq.items() if k not in table}
         print(f"{len(uniq)} shapes missing from the table", flush=True)

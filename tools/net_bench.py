@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--early", type=int, default=1, help="GEMM weight tiles requested before the PDL wait")
+    ap.add_argument("--kb2", type=int, default=-1, help="GEMM 2-k-block TMA boxes (drs_set_gemm_kb2; -1 = default)")
     ap.add_argument("--attn", type=int, default=2, help="attention variant (drs_set_attn_split)")
     ap.add_argument("--tail", type=int, default=0, help="attention tail split (drs_set_attn_tail_split)")
     a = ap.parse_args()
@@ -26,6 +27,8 @@ def main():
     _lib.lib().drs_set_pdl(a.pdl)
     _lib.lib().drs_set_early_weights(a.early)
     _lib.lib().drs_set_attn_split(a.attn)
+    if a.kb2 >= 0:
+        _lib.lib().drs_set_gemm_kb2(a.kb2)
     _lib.lib().drs_set_attn_tail_split(a.tail)
     dev = torch.device("cuda", 0)
     if a.net == "dit":

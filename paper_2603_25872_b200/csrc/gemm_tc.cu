@@ -830,6 +830,8 @@ struct PairSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / 2) * kBK * 2;         // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kAOff = 0;                            // A tiles of all stages, then B (as GemmSmem)
+  static constexpr int kBOff = kStages * kABytes;
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
   static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;
@@ -842,6 +844,14 @@ __device__ __forceinline__ void tma_load_2d_pair(const void* tmap, uint64_t* bar
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];"
       :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                                 int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
 }
 __device__ __forceinline__ void tma_load_4d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                                  int32_t c2, int32_t c3) {
@@ -875,6 +885,34 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {   // arrive 
 }
 __device__ __forceinline__ void pair_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// A operand of a pair CTA's ring slot: kpb k-blocks (conv: one 4-D box per k-block,
+// a missing 2nd block of the last slot reloads a valid box whose MMA is skipped;
+// otherwise one 2-D box, or one 3-D box carrying 2 k-blocks)
+__device__ __forceinline__ void pair_load_a(const CUtensorMap* tmap_a, uint64_t* bar, uint8_t* sa, int a_bytes, int kb,
+                                            int num_kb, int m0, const ConvGeom& cv, int kpb) {
+  if (cv.on) {
+    for (int q = 0; q < kpb; ++q) {
+      const int k = min(kb + q, num_kb - 1);
+      const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
+      const int ky = tap / 3, kx = tap - ky * 3;
+      const int hw = cv.H * cv.W;
+      const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+      tma_load_4d_pair(tmap_a, bar, sa + q * a_bytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
+    }
+  } else if (kpb == 2) {
+    tma_load_3d_pair(tmap_a, bar, sa, 0, m0, kb);
+  } else {
+    tma_load_2d_pair(tmap_a, bar, sa, kb * kBK, m0);
+  }
+}
+__device__ __forceinline__ void pair_load_b(const CUtensorMap* tmap_b, uint64_t* bar, uint8_t* sb, int kb, int row,
+                                            int kpb) {
+  if (kpb == 2)
+    tma_load_3d_pair(tmap_b, bar, sb, 0, row, kb);
+  else
+    tma_load_2d_pair(tmap_b, bar, sb, kb * kBK, row);
 }
 
 template <int BN, int kStages, int kEpi>
@@ -928,15 +966,18 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
     if (tc::elect_one()) {
       // weight (B) halves of the first kStages k-blocks before the PDL wait (as in
       // gemm_bf16_tc_kernel): they never depend on a predecessor kernel
+      // kb2: ring slots of 2 stages / 2 k-blocks per TMA box (see gemm_bf16_tc_kernel)
+      const int kpb = ep.kb2 ? 2 : 1;
+      const int nst = kStages / kpb;
       int pre = 0;
       if (t0 < num_tiles) {
         const int pmt = t0 % pm_tiles, nt = t0 / pm_tiles;
-        pre = ep.early_b ? min(kStages, num_kb) : 0;
+        pre = ep.early_b ? min(nst, (num_kb + kpb - 1) / kpb) : 0;
         for (int j = 0; j < pre; ++j) {
-          uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
-          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * S::kStageBytes);
-          tma_load_2d_pair(&tmap_b, &full_bar[j], sb, j * kBK,
-                           nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+          uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
+          pair_load_b(&tmap_b, &full_bar[j], sb, j * kpb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                      kpb);
         }
       }
       pdl_wait();
@@ -945,31 +986,25 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
       for (int tile = t0; tile < num_tiles; tile += tstep) {
         const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
         const int m0 = (pmt * 2 + rank) * kBM;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          const bool b_done = tile == t0 && kb < pre;
+        for (int kb = 0, j = 0; kb < num_kb; kb += kpb, ++j) {
+          const bool b_done = tile == t0 && j < pre;
           if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * S::kStageBytes;
-          uint8_t* sb = sa + S::kABytes;
-          if (rank == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
-          if (cv.on) {
-            const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
-            const int ky = tap / 3, kx = tap - ky * 3;
-            const int hw = cv.H * cv.W;
-            const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-            tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
-          } else {
-            tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
-          }
+          uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
+          uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
+          if (rank == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
+          pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
           if (!b_done)
-            tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
-                             nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+            pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                        kpb);
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (rank == 0) {
+      const int kpb = ep.kb2 ? 2 : 1;
+      const int nst = kStages / kpb;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -978,21 +1013,22 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
         tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < num_kb; kb += kpb) {
           tc::mbar_wait(&full_bar[stage], phase);
           tc::tc_fence_after();
           if (tc::elect_one()) {
-            const uint8_t* sa = smem + stage * S::kStageBytes;
-            const uint64_t da = tc::smem_desc_sw128(sa);
-            const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+            for (int q = 0; q < kpb && kb + q < num_kb; ++q) {
+              const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
+              const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              mma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < kBK / 16; ++k)
+                mma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > 0 || k > 0) ? 1u : 0u);
+            }
             mma_commit_pair(&empty_bar[stage]);
-            if (kb == num_kb - 1) mma_commit_pair(&tfull_bar[acc]);
+            if (kb + kpb >= num_kb) mma_commit_pair(&tfull_bar[acc]);
           }
           __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -1135,56 +1171,53 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   if (warp == 0) {
     if (tc::elect_one()) {
       // weight (B) halves of the first kStages k-blocks before the PDL wait
-      const int pre = ep.early_b ? max(0, min(kStages, kb1 - kb0)) : 0;
+      const int kpb = ep.kb2 ? 2 : 1;
+      const int nst = kStages / kpb;
+      const int pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
       for (int j = 0; j < pre; ++j) {
-        uint8_t* sb = smem + j * S::kStageBytes + S::kABytes;
-        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * S::kStageBytes);
-        tma_load_2d_pair(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK,
-                         nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
+        uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
+        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
+        pair_load_b(&tmap_b, &full_bar[j], sb, kb0 + j * kpb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                    kpb);
       }
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const bool b_done = kb - kb0 < pre;
+      for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
+        const bool b_done = j < pre;
         if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * S::kStageBytes;
-        uint8_t* sb = sa + S::kABytes;
-        if (half == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
-        if (cv.on) {
-          const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
-          const int ky = tap / 3, kx = tap - ky * 3;
-          const int hw = cv.H * cv.W;
-          const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-          tma_load_4d_pair(&tmap_a, &full_bar[stage], sa, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
-        } else {
-          tma_load_2d_pair(&tmap_a, &full_bar[stage], sa, kb * kBK, m0);
-        }
+        uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
+        uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
+        if (half == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
+        pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
         if (!b_done)
-          tma_load_2d_pair(&tmap_b, &full_bar[stage], sb, kb * kBK,
-                           nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM));
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+          pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                      kpb);
+        if (++stage == nst) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     if (half == 0) {
+      const int kpb = ep.kb2 ? 2 : 1;
+      const int nst = kStages / kpb;
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; kb += kpb) {
         tc::mbar_wait(&full_bar[stage], phase);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          const uint8_t* sa = smem + stage * S::kStageBytes;
-          const uint64_t da = tc::smem_desc_sw128(sa);
-          const uint64_t db = tc::smem_desc_sw128(sa + S::kABytes);
+          for (int q = 0; q < kpb && kb + q < kb1; ++q) {
+            const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
+            const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            mma_bf16_pair(tmem_base, da + 2 * k, db + 2 * k, kIdesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16_pair(tmem_base, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+          }
           mma_commit_pair_mask(&empty_bar[stage], pair_mask);
-          if (kb == kb1 - 1) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
+          if (kb + kpb >= kb1) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == nst) { stage = 0; phase ^= 1; }
       }
       if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
         if (tc::elect_one()) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
@@ -1630,7 +1663,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
     if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C, cs)) return DRS_ERR_CUDA;
     cv = ConvGeom{1, C / 64, H, W, 0, 0, cs};
   }
-  // kb2 (1-SM kernels only, K % 64 == 0): one TMA box carries 2 k-blocks -- half the
+  // kb2 (K % 64 == 0): one TMA box carries 2 k-blocks -- half the
   // TMA operations, whose per-op issue cost (~190 clk from one thread) bounds the
   // operand stream of small tiles (tools/micro/tma_kb2.cu)
   const bool kb2_ok = (g->kbox == 2 || (g->kbox == 0 && gemm_kb2_mode())) && K % kBK == 0 && !hsm;
@@ -1665,10 +1698,10 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM)) &&
                     (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
   const int64_t b_rows = N + (g->b_img_rows > 0 ? g->b_img_off : 0);
-  if (kb2_ok && !pair) {
+  if (kb2_ok) {
     ep.kb2 = 1;
     if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
-    if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, bn)) return DRS_ERR_CUDA;
+    if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn)) return DRS_ERR_CUDA;
   } else if (!make_tmap(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn)) {
     return DRS_ERR_CUDA;
   }

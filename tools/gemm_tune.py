@@ -115,8 +115,7 @@ def tune_shape(desc, dev, reps, cold=False):
 
 
 def tune_kbox(desc, cfg, dev, reps, cold=False):
-    """Time the table's (bn, split) for this shape with 1 and 2 k-blocks per TMA box
-    (1-SM kernels; pair entries keep 1)."""
+    """Time the table's (bn, split, pair) for this shape with 1 and 2 k-blocks per TMA box."""
     import torch
     from paper_2603_25872_b200.netops import linear
     M, N, K, act, res_f32, has_res, out_f32, conv = desc
@@ -138,11 +137,11 @@ def tune_kbox(desc, cfg, dev, reps, cold=False):
     out = torch.empty(M, n_out, device=dev, dtype=torch.float32 if out_f32 else torch.bfloat16)
     res = torch.randn(M, n_out, device=dev, dtype=torch.float32 if res_f32 else torch.bfloat16) if has_res else None
     bias = torch.randn(N, device=dev)
-    bn, sp = cfg[0], cfg[1]
+    bn, sp, pr = cfg[0], cfg[1], bool(cfg[2]) if len(cfg) > 2 else False
     t = {}
     for kbox in (1, 2):
         run = lambda kbox=kbox: linear(x, wnext(), bias=bias, act=act, residual=res, out=out, bn=bn,   # noqa: E731
-                                       split=sp, conv=conv, pair=False, kbox=kbox)
+                                       split=sp, conv=conv, pair=pr, kbox=kbox)
         t[kbox] = time_config(run, reps)
     return t
 
@@ -157,7 +156,7 @@ def main():
     ap.add_argument("--merge", action="store_true", help="update the existing table instead of replacing it")
     ap.add_argument("--only-missing", action="store_true", help="with --merge: tune only shapes not in the table")
     ap.add_argument("--kbox", action="store_true",
-                    help="keep each entry's (bn, split, pair); choose 1 or 2 k-blocks per TMA box for 1-SM entries")
+                    help="keep each entry's (bn, split, pair); choose 1 or 2 k-blocks per TMA box")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import netops
@@ -182,14 +181,14 @@ def main():
         tot1 = tot_sel = 0.0
         for key, d in sorted(uniq.items()):
             cfg = table.get(key)
-            if cfg is None or (len(cfg) > 2 and cfg[2]) or d[2] % 64:
+            if cfg is None or d[2] % 64:
                 continue
-            t = tune_kbox(d, cfg[:2], dev, a.reps, a.cold)
+            t = tune_kbox(d, cfg[:3], dev, a.reps, a.cold)
             kbox = 2 if t[2] < t[1] * 0.98 else 1
             table[key] = list(cfg[:3]) + [kbox] if len(cfg) > 2 else list(cfg[:2]) + [0, kbox]
             tot1 += t[1]
             tot_sel += t[kbox]
-            print(f"{key:24s} bn={cfg[0]:3d} split={cfg[1]}  kbox1 {t[1]:8.1f} us  kbox2 {t[2]:8.1f} us -> {kbox}",
+            print(f"{key:24s} bn={cfg[0]:3d} split={cfg[1]} pair={cfg[2] if len(cfg) > 2 else 0}  kbox1 {t[1]:8.1f} us  kbox2 {t[2]:8.1f} us -> {kbox}",
                   flush=True)
         print(f"kbox pass: sum {tot1:.0f} us (1 k-block per box) -> {tot_sel:.0f} us (selected)")
         uniq = {}

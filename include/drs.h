@@ -177,8 +177,9 @@ int drs_set_pdl(int on);
 /* 1 (default): GEMM producers request their first weight (B) tiles before the
  * PDL wait, overlapping the cold weight stream with the predecessor kernel. */
 int drs_set_early_weights(int on);
-/* Measurement switch: 1 = the 1-SM GEMM kernels load two k-blocks per TMA box (3-D tensor maps,
- * K % 64 == 0), halving the TMA operations of the operand stream; 0 = one k-block per box. */
+/* Default k-blocks per GEMM TMA box for calls whose drs_gemm_args.kbox is 0: 0 -> 1 (default),
+ * 1 / 2 -> 2, 4 -> 4 (3-D tensor maps, K % 64 == 0; 4 only for 8-stage tiles).  Fewer, larger TMA
+ * operations: the per-op issue cost bounds the operand stream of small tiles. */
 int drs_set_gemm_kb2(int on);
 
 #ifdef __cplusplus

@@ -80,8 +80,8 @@ typedef struct drs_gemm_args {
    * a stride-2, pad-1 3x3 conv over a 2H x 2W input; the A box is loaded with TMA
    * element stride 2 -- downsamplers without an im2col copy). */
   int conv_stride;
-  /* k-blocks (of 64) per TMA box in the 1-SM kernels: 0 = library default
-   * (drs_set_gemm_kb2), 1, or 2 (3-D [K/64][rows][64] tensor maps, K % 64 == 0). */
+  /* k-blocks (of 64) per TMA box: 0 = library default (drs_set_gemm_kb2), 1, 2 or 4
+   * (3-D [K/64][rows][64] tensor maps, K % 64 == 0; 4 falls back to 2 for tiles with < 8 stages). */
   int kbox;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);

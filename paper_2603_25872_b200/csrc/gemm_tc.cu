@@ -145,8 +145,8 @@ struct EpiParams {
   void* out2;               // kEpi 4: a bf16 copy of the (fp32) output, row stride ldo2
   int64_t ldo2;
   int early_b;              // 1: weight tiles of the first stages requested before the PDL wait
-  int kb2;                  // 1: A / B tensor maps are 3-D [K/64][rows][64] views and one TMA box
-                            //    carries 2 k-blocks (2 ring stages: one full/empty barrier pair)
+  int kpb;                  // k-blocks per ring slot / TMA box: 1, or 2 / 4 with A / B tensor maps that are
+                            //    3-D [K/64][rows][64] views (kpb stages share one full/empty barrier pair)
 };
 
 // kEpi 4: the finished row segment (32 values) also goes to the bf16 copy
@@ -594,7 +594,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       // stage's full barrier also expects the A bytes, which follow the wait).
       // kb2: a ring slot ("super-stage") is 2 consecutive stages = 2 k-blocks,
       // loaded by one 3-D box per operand (conv A: one 4-D box per k-block)
-      const int kpb = ep.kb2 ? 2 : 1;
+      const int kpb = ep.kpb;
       const int nst = kStages / kpb;
       int pre = 0;
       if ((int)blockIdx.x < num_tiles) {
@@ -605,8 +605,8 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
         for (int j = 0; j < pre; ++j) {
           uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
           tc::mbar_arrive_expect_tx(&full_bar[j], kpb * S::kStageBytes);
-          if (kpb == 2)
-            tma_load_3d(&tmap_b, &full_bar[j], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb0 + 2 * j);
+          if (kpb > 1)
+            tma_load_3d(&tmap_b, &full_bar[j], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb0 + j * kpb);
           else
             tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
         }
@@ -635,13 +635,13 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
               const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
               tma_load_4d(&tmap_a, &full_bar[stage], sa + q * S::kABytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
             }
-          } else if (kpb == 2) {
+          } else if (kpb > 1) {
             tma_load_3d(&tmap_a, &full_bar[stage], sa, 0, mt * kBM, kb);
           } else {
             tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
           }
           if (!b_done) {
-            if (kpb == 2)
+            if (kpb > 1)
               tma_load_3d(&tmap_b, &full_bar[stage], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb);
             else
               tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
@@ -652,7 +652,7 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    const int kpb = ep.kb2 ? 2 : 1;
+    const int kpb = ep.kpb;
     const int nst = kStages / kpb;
     int stage = 0;
     uint32_t phase = 0;
@@ -901,7 +901,7 @@ __device__ __forceinline__ void pair_load_a(const CUtensorMap* tmap_a, uint64_t*
       const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
       tma_load_4d_pair(tmap_a, bar, sa + q * a_bytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
     }
-  } else if (kpb == 2) {
+  } else if (kpb > 1) {
     tma_load_3d_pair(tmap_a, bar, sa, 0, m0, kb);
   } else {
     tma_load_2d_pair(tmap_a, bar, sa, kb * kBK, m0);
@@ -909,7 +909,7 @@ __device__ __forceinline__ void pair_load_a(const CUtensorMap* tmap_a, uint64_t*
 }
 __device__ __forceinline__ void pair_load_b(const CUtensorMap* tmap_b, uint64_t* bar, uint8_t* sb, int kb, int row,
                                             int kpb) {
-  if (kpb == 2)
+  if (kpb > 1)
     tma_load_3d_pair(tmap_b, bar, sb, 0, row, kb);
   else
     tma_load_2d_pair(tmap_b, bar, sb, kb * kBK, row);
@@ -967,7 +967,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
       // weight (B) halves of the first kStages k-blocks before the PDL wait (as in
       // gemm_bf16_tc_kernel): they never depend on a predecessor kernel
       // kb2: ring slots of 2 stages / 2 k-blocks per TMA box (see gemm_bf16_tc_kernel)
-      const int kpb = ep.kb2 ? 2 : 1;
+      const int kpb = ep.kpb;
       const int nst = kStages / kpb;
       int pre = 0;
       if (t0 < num_tiles) {
@@ -1003,7 +1003,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (rank == 0) {
-      const int kpb = ep.kb2 ? 2 : 1;
+      const int kpb = ep.kpb;
       const int nst = kStages / kpb;
       int stage = 0;
       uint32_t phase = 0;
@@ -1171,7 +1171,7 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   if (warp == 0) {
     if (tc::elect_one()) {
       // weight (B) halves of the first kStages k-blocks before the PDL wait
-      const int kpb = ep.kb2 ? 2 : 1;
+      const int kpb = ep.kpb;
       const int nst = kStages / kpb;
       const int pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
       for (int j = 0; j < pre; ++j) {
@@ -1198,7 +1198,7 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     }
   } else if (warp == 1) {
     if (half == 0) {
-      const int kpb = ep.kb2 ? 2 : 1;
+      const int kpb = ep.kpb;
       const int nst = kStages / kpb;
       int stage = 0;
       uint32_t phase = 0;
@@ -1316,23 +1316,24 @@ static bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t col
 // 2 W x 2 rows input elements traversed with element stride 2, i.e. it loads the
 // same 128 x 64-channel tile of pixels (s y + ky - 1, s x + kx - 1).
 // 3-D view [K/64][rows][64] of a K-contiguous bf16 matrix (K % 64 == 0): a
-// {64, box_rows, 2} box is two consecutive k-block tiles (kb2 mode)
-static bool make_tmap_kb2(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+// {64, box_rows, kpb} box is kpb consecutive k-block tiles (kpb = 2 or 4)
+static bool make_tmap_kb2(CUtensorMap* m, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows,
+                          int kpb) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)rows, (cuuint64_t)(K / kBK)};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(kBK * 2)};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 2};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, (cuuint32_t)kpb};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// drs_set_gemm_kb2: 1-SM kernels load 2 k-blocks per TMA box when K % 64 == 0
+// drs_set_gemm_kb2: default k-blocks per TMA box (1, 2 or 4) for calls with kbox == 0
 inline int& gemm_kb2_mode() {
-  static int on = 0;
-  return on;
+  static int kpb = 1;
+  return kpb;
 }
 
 static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
@@ -1531,6 +1532,12 @@ static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M
 }
 
 
+// stages of the instantiation gemm_dispatch picks (kept in sync with it)
+static int gemm_stages(int bn, bool pair, int split) {
+  if (pair) return bn == 64 || bn == 128 ? 8 : (bn == 160 ? 7 : 6);
+  return bn == 64 ? 8 : (bn == 128 ? 6 : (bn == 160 ? 5 : 4));
+}
+
 template <int kEpi>
 static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
                          int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
@@ -1666,7 +1673,9 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   // kb2 (K % 64 == 0): one TMA box carries 2 k-blocks -- half the
   // TMA operations, whose per-op issue cost (~190 clk from one thread) bounds the
   // operand stream of small tiles (tools/micro/tma_kb2.cu)
-  const bool kb2_ok = (g->kbox == 2 || (g->kbox == 0 && gemm_kb2_mode())) && K % kBK == 0 && !hsm;
+  int kpb = g->kbox == 0 ? gemm_kb2_mode() : g->kbox;
+  if (kpb != 1 && kpb != 2 && kpb != 4) return DRS_ERR_VALUE;
+  if (K % kBK || hsm) kpb = 1;
   if (!g->conv_C) {
     if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
   }
@@ -1676,7 +1685,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   }
   EpiParams ep{g->C, g->ldc, g->bias, g->residual, g->ldr, g->res_f32, g->colscale, g->cs_group, g->cs_ld,
                g->rowbias, g->rb_group, g->rb_ld, g->alpha, g->act, g->out_f32, 0, g->hs_valid, 0, g->out2, g->ldo2,
-               early_weights_enabled(), 0};
+               early_weights_enabled(), 1};
   // staged TMA store whenever the output layout allows it (16-byte aligned rows)
   OutMaps tcm;
   memset(&tcm, 0, sizeof(tcm));
@@ -1698,10 +1707,12 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM)) &&
                     (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
   const int64_t b_rows = N + (g->b_img_rows > 0 ? g->b_img_off : 0);
-  if (kb2_ok) {
-    ep.kb2 = 1;
-    if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
-    if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn)) return DRS_ERR_CUDA;
+  // a ring of kStages / kpb slots needs >= 2 slots: 4 k-blocks per box only with 8-stage instantiations
+  if (kpb == 4 && gemm_stages(bn, pair, split) < 8) kpb = 2;
+  ep.kpb = kpb;
+  if (kpb > 1) {
+    if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM, kpb)) return DRS_ERR_CUDA;
+    if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn, kpb)) return DRS_ERR_CUDA;
   } else if (!make_tmap(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn)) {
     return DRS_ERR_CUDA;
   }
@@ -1732,6 +1743,6 @@ extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
 }
 
 extern "C" int drs_set_gemm_kb2(int on) {
-  drs::gemm_kb2_mode() = on ? 1 : 0;
+  drs::gemm_kb2_mode() = on == 4 ? 4 : (on ? 2 : 1);
   return DRS_OK;
 }

@@ -6,10 +6,10 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=[0, 1], ids=["kb1", "kb2"])
+@pytest.fixture(autouse=True, params=[0, 1, 4], ids=["kb1", "kb2", "kb4"])
 def kb2_mode(request):
-    """Every GEMM test runs with one k-block per TMA box and with two (kb2 mode:
-    3-D [K/64][rows][64] tensor maps, 2-stage ring slots; 1-SM kernels, K % 64 == 0)."""
+    """Every GEMM test runs with one, two and four k-blocks per TMA box (3-D
+    [K/64][rows][64] tensor maps, ring slots of 2 / 4 stages; K % 64 == 0)."""
     from paper_2603_25872_b200 import _lib
     _lib.lib().drs_set_gemm_kb2(request.param)
     yield request.param

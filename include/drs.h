@@ -178,8 +178,8 @@ int drs_set_pdl(int on);
  * PDL wait, overlapping the cold weight stream with the predecessor kernel. */
 int drs_set_early_weights(int on);
 /* Default k-blocks per GEMM TMA box for calls whose drs_gemm_args.kbox is 0: 0 -> 1 (default),
- * 1 / 2 -> 2, 4 -> 4 (3-D tensor maps, K % 64 == 0; 4 only for 8-stage tiles).  Fewer, larger TMA
- * operations: the per-op issue cost bounds the operand stream of small tiles. */
+ * otherwise 2 (separate kernel instantiations with 3-D tensor maps, K % 64 == 0).  Fewer, larger
+ * TMA operations: the per-op issue cost bounds the operand stream of small tiles. */
 int drs_set_gemm_kb2(int on);
 
 #ifdef __cplusplus

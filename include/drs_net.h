@@ -80,8 +80,8 @@ typedef struct drs_gemm_args {
    * a stride-2, pad-1 3x3 conv over a 2H x 2W input; the A box is loaded with TMA
    * element stride 2 -- downsamplers without an im2col copy). */
   int conv_stride;
-  /* k-blocks (of 64) per TMA box: 0 = library default (drs_set_gemm_kb2), 1, 2 or 4
-   * (3-D [K/64][rows][64] tensor maps, K % 64 == 0; 4 falls back to 2 for tiles with < 8 stages). */
+  /* k-blocks (of 64) per TMA box: 0 = library default (drs_set_gemm_kb2), 1 or 2
+   * (3-D [K/64][rows][64] tensor maps, K % 64 == 0; 4 is accepted and runs as 2). */
   int kbox;
 } drs_gemm_args;
 int drs_gemm(const drs_gemm_args* args, void* stream);
@@ -131,11 +131,8 @@ int drs_gemv(const void* x, int64_t ldx, const void* w, int64_t ldw, const float
              int ctas_per_sm /* 0: 4 per SM; 1: leaves room for co-resident GEMM CTAs */, void* stream);
 
 /* Measurement switch: 0 = attention with one MMA warp, 1 = separate S and PV MMA issuer warps,
- * 2 (default) = 1 + the softmax on the paired FP32 pipe, 3 = 2 + two P buffers per softmax set (d <= 64). */
+ * 2 (default) = 1 + the softmax on the paired FP32 pipe (FFMA2 / FADD2). */
 int drs_set_attn_split(int on);
-/* Measurement switch: 1 = the (query tile, head, image) items of the last partial wave of an
- * attention launch run as two key-range halves (combined by the second to finish); 0 (default). */
-int drs_set_attn_tail_split(int on);
 
 /* DiT helpers */
 int drs_timestep_embedding(const float* t, int n, int dim, float max_period, void* out_bf16, void* stream);

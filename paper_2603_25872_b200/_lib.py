@@ -127,7 +127,6 @@ _SIGS = {
     "drs_set_noise_resolve": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_gn_mode": (ctypes.c_int, [ctypes.c_int]),
     "drs_set_attn_split": (ctypes.c_int, [ctypes.c_int]),
-    "drs_set_attn_tail_split": (ctypes.c_int, [ctypes.c_int]),
     # include/drs_net.h
     "drs_gemm_bf16": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -2,8 +2,7 @@
 //
 //   O[b, q, h, :] = softmax_k( Q[b, q, h, :] . K[b, k, h, :] * scale ) V[b, k, h, :]
 //
-// One CTA per (128-query tile, head, image) item -- or per key half of an item
-// in the tail split (below).  Warp roles (352 threads, default build):
+// One CTA per (128-query tile, head, image).  Warp roles (352 threads, default build):
 //   warp 0      TMA producer: Q once, then K / V tiles of 128 keys into two
 //               rings (mbarrier full/empty)
 //   warp 1      TMEM allocator + S issuer: S_j = Q K_j^T (M=128, N=128, K=DP)
@@ -21,10 +20,6 @@
 //               combined in the epilogue.  d > 128: one set, two warps per
 //               quadrant split each tile's key columns (row max exchanged
 //               through shared memory).
-// Tail split: when the items leave a last partial wave of t <= SMs/2 CTAs (and
-// there are >= 16 key tiles), those t items run as 2t key-half CTAs; both
-// halves write (O, m, l) to a device workspace and the second to finish
-// combines them (in half order, so the bits do not depend on arrival order).
 // Operands: Q, K and (row-major) V through 3-D tensor maps (elem, head, row),
 // so head dims that are not multiples of 64 are zero-filled by TMA up to DP;
 // V row-major is the MN-major B operand of the PV MMA; V^T (channels x keys)
@@ -45,18 +40,6 @@ constexpr int kAQ = 128;       // queries per CTA
 constexpr int kAK = 128;       // keys per tile
 constexpr int kAttnTcThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 softmax (2 per TMEM quadrant)
 
-// Tail split (split-KV of the last partial wave): when the (query tile, head,
-// image) items leave a last wave of t <= SMs/2 CTAs, those t items run as 2t
-// half-items over the two halves of the key tiles; both halves write their
-// unnormalised O, row max and row sum here, and the one that arrives second
-// (per-item arrival counter, reset by it) combines both and stores the output.
-// Stream-ordered use only (one workspace per device, as for any kernel that
-// keeps state in device globals).
-constexpr int kTailSlots = 80;
-constexpr int kPartFloats = kAQ * 128 + 2 * kAQ;   // O rows (<= 128 channels), then m, l
-__device__ float g_attn_part[kTailSlots * 2 * kPartFloats];
-__device__ int g_attn_cnt[kTailSlots];          // arrivals per tail item
-
 // Debug aid: when set (drs_attention_tc_debug), CTAs record per-role progress
 // markers into host-mapped memory the CPU can read while a launch is stuck.
 __device__ int* g_attn_trace = nullptr;
@@ -72,7 +55,7 @@ __device__ int* g_attn_trace = nullptr;
   } while (0)
 #endif
 
-template <int DP, int PB = 2>
+template <int DP>
 struct AttnSmem {
   // independent softmax sets: with two, set s owns whole S rows of the key
   // tiles j = s, s+2, ... and its own O accumulator (TMEM: S0, S1, O0, O1 =
@@ -85,23 +68,18 @@ struct AttnSmem {
   static constexpr int kVBytes = DP * kAK * 2;
   static constexpr int kPBytes = kAQ * kAK * 2;
   static constexpr int kRedBytes = kSets == 1 ? 2 * kAQ * 4 : 0;   // per-tile row-max exchange (1 set)
-  // P buffers: 2 = one per set (P_{j+2} waits for PV_j), 4 = two per set
-  // (P_{j+2} is written while PV_j still runs; P_{j+4} waits for PV_j)
-  static_assert(PB == 2 || (PB == 4 && kSets == 2), "4 P buffers need two softmax sets");
-  static constexpr int kNumBars = 22 + 2 * PB;
+  static constexpr int kNumBars = 26;
   // separate K and V rings, as deep as 227 KB allows (<= 4): K_{j+s} loads as
   // soon as S_j has consumed its slot, V_{j+s} once PV_j has
-  static constexpr int kFixed = kQBytes + PB * kPBytes + kRedBytes + kNumBars * 8 + 1024;
+  static constexpr int kFixed = kQBytes + 2 * kPBytes + kRedBytes + kNumBars * 8 + 1024;
   static constexpr int kFit = (227 * 1024 - kFixed) / (kKBytes + kVBytes);
-  static constexpr int kFitTiles = (227 * 1024 - kFixed) / kKBytes;      // K and V tiles are the same size
-  static constexpr int kKStages = PB == 2 ? (kFit > 4 ? 4 : kFit) : ((kFitTiles + 1) / 2 > 4 ? 4 : (kFitTiles + 1) / 2);
-  static constexpr int kVStages = PB == 2 ? kKStages : (kFitTiles / 2 > 4 ? 4 : kFitTiles / 2);
-  static_assert(kKStages >= 1 && kVStages >= 1, "attention tile does not fit in shared memory");
+  static constexpr int kStages = kFit > 4 ? 4 : kFit;
+  static_assert(kStages >= 1, "attention tile does not fit in shared memory");
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;
-  static constexpr int kV = kK + kKStages * kKBytes;
-  static constexpr int kP = kV + kVStages * kVBytes;       // P buffer j % PB
-  static constexpr int kRed = kP + PB * kPBytes;
+  static constexpr int kV = kK + kStages * kKBytes;
+  static constexpr int kP = kV + kStages * kVBytes;        // P double-buffered (buffer j & 1)
+  static constexpr int kRed = kP + 2 * kPBytes;
   static constexpr int kBar = kRed + kRedBytes;
   // >= 116 KB so two CTAs never share an SM: each allocates all 512 TMEM columns
   static constexpr int kRaw = kBar + kNumBars * 8 + 1024;
@@ -170,23 +148,6 @@ __device__ __forceinline__ void ex2_poly2(float2 x, float& y0, float& y1) {
   y0 = __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
   y1 = __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
 }
-// 32 O columns of this thread's row from TMEM, the two sets' accumulators
-// combined with their max-correction factors (f1 unused with one set / one tile)
-__device__ __forceinline__ void attn_o_row(uint32_t taddr, int dp, bool two, float f0, float f1, uint32_t (&r0)[32]) {
-  tc::tmem_ld32(taddr, r0);
-  if (two) {
-    uint32_t r1[32];
-    tc::tmem_ld32(taddr + dp, r1);                 // the second set's O accumulator
-    tmem_ld_wait_regs(r0);
-    reg_pin(r1);
-#pragma unroll
-    for (int e = 0; e < 32; ++e) r0[e] = __float_as_uint(fmaf(__uint_as_float(r0[e]), f0, __uint_as_float(r1[e]) * f1));
-  } else {
-    tmem_ld_wait_regs(r0);
-#pragma unroll
-    for (int e = 0; e < 32; ++e) r0[e] = __float_as_uint(__uint_as_float(r0[e]) * f0);
-  }
-}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2) {
@@ -220,42 +181,31 @@ __device__ __forceinline__ int sw128_off(int row, int c) {
 // (ncu: the softmax warps spent 21.5 % of their samples waiting for S tiles).
 // X2: the exps' argument scaling, the poly exps and the row sums on the paired
 // FP32 pipe (FFMA2 / FADD2: half the issue slots of the scalar loop)
-template <int DP, int NPOLY, bool VROW, bool SPLIT, bool X2 = false, int PB = 2>
+template <int DP, int NPOLY, bool VROW, bool SPLIT, bool X2 = false>
 __global__ void __launch_bounds__(SPLIT ? kAttnTcThreads + 32 : kAttnTcThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
-               int Lq, int Lk, int d, int vt_img, float scale_log2, int H, int items_full) {
-  using S = AttnSmem<DP, PB>;
-  constexpr int kKSt = S::kKStages;
-  constexpr int kVSt = S::kVStages;
+               int Lq, int Lk, int d, int vt_img, float scale_log2) {
+  using S = AttnSmem<DP>;
+  constexpr int kSt = S::kStages;
   constexpr int kSets = S::kSets;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* q_full = bars;                 // 1
-  uint64_t* k_full = bars + 1;             // kKSt (<= 4)
-  uint64_t* k_empty = bars + 5;            // kKSt  (released by S_j)
-  uint64_t* v_full = bars + 9;             // kVSt
-  uint64_t* v_empty = bars + 13;           // kVSt  (released by PV_j)
+  uint64_t* k_full = bars + 1;             // kSt (<= 4)
+  uint64_t* k_empty = bars + 5;            // kSt   (released by S_j)
+  uint64_t* v_full = bars + 9;             // kSt
+  uint64_t* v_empty = bars + 13;           // kSt   (released by PV_j)
   uint64_t* s_full = bars + 17;            // 2 (per S buffer)
-  uint64_t* s_free = bars + 19;            // 2 (S buffer read into registers: S_{j+2} may overwrite)
-  uint64_t* p_full = bars + 21;            // PB (per P buffer; one arrival per softmax warp of the tile)
-  uint64_t* o_done = bars + 21 + PB;       // PB (per P buffer: PV_j committed to o_done[j % PB])
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21 + 2 * PB);
+  uint64_t* p_full = bars + 19;            // 2 (per P buffer; one arrival per softmax warp of the tile)
+  uint64_t* o_done = bars + 21;            // 2 (per P buffer: PV_j committed to o_done[j & 1])
+  uint64_t* s_free = bars + 23;            // 2 (S buffer read into registers: S_{j+2} may overwrite)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // item = (query tile, head, image), query tile fastest; CTAs past items_full
-  // are the halves of the tail items (key tiles [0, n/2) and [n/2, n))
-  const int qtiles = (Lq + kAQ - 1) / kAQ;
-  const int n_all = (Lk + kAK - 1) / kAK;
-  int item = blockIdx.x, half = -1;
-  if (item >= items_full) {
-    half = (item - items_full) & 1;
-    item = items_full + ((item - items_full) >> 1);
-  }
-  const int q0 = (item % qtiles) * kAQ, h = (item / qtiles) % H, b = item / (qtiles * H);
-  const int t0 = half == 1 ? n_all / 2 : 0;                       // first key tile of this CTA
-  const int n_tiles = half < 0 ? n_all : (half == 0 ? n_all / 2 : n_all - n_all / 2);
+  const int q0 = blockIdx.x * kAQ, h = blockIdx.y, b = blockIdx.z;
+  const int n_tiles = (Lk + kAK - 1) / kAK;
   constexpr uint32_t kIdescS = tc::idesc_bf16_f32(128, kAK);
   constexpr uint32_t kIdescO = VROW ? tc::idesc_bf16_f32_bmn(128, DP) : tc::idesc_bf16_f32(128, DP);
 
@@ -265,14 +215,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     tc::tma_prefetch(&tm_vt);
     tc::tma_prefetch(&tm_o);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < kKSt; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1); }
-    for (int s = 0; s < kVSt; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
+    for (int s = 0; s < kSt; ++s) {
+      tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1);
+      tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_free[i], kSets == 2 ? 4 : 8);
-    }
-    for (int i = 0; i < PB; ++i) {
       tc::mbar_init(&p_full[i], kSets == 2 ? 4 : 8);
+      tc::mbar_init(&s_free[i], kSets == 2 ? 4 : 8);
       tc::mbar_init(&o_done[i], 1);
     }
     tc::fence_barrier_init();
@@ -297,27 +247,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       for (int a = 0; a < S::kAtoms; ++a)
         tma_load_3d(&tm_q, q_full, sQ + a * (kAQ * 128), a * 64, h, b * Lq + q0);
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % kKSt;
-        tc::mbar_wait(&k_empty[st], ((j / kKSt) & 1) ^ 1);
+        const int st = j % kSt;
+        tc::mbar_wait(&k_empty[st], ((j / kSt) & 1) ^ 1);
         ATTN_TRACE(1, 100 + j);
         tc::mbar_arrive_expect_tx(&k_full[st], S::kKBytes);
         uint8_t* k_dst = sK + st * S::kKBytes;
         for (int a = 0; a < S::kAtoms; ++a)
-          tma_load_3d(&tm_k, &k_full[st], k_dst + a * (kAK * 128), a * 64, h, b * Lk + (t0 + j) * kAK);
+          tma_load_3d(&tm_k, &k_full[st], k_dst + a * (kAK * 128), a * 64, h, b * Lk + j * kAK);
       }
     } else if (lane == 1) {
       for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % kVSt;
-        tc::mbar_wait(&v_empty[st], ((j / kVSt) & 1) ^ 1);
+        const int st = j % kSt;
+        tc::mbar_wait(&v_empty[st], ((j / kSt) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&v_full[st], S::kVBytes);
         uint8_t* v_dst = sV + st * S::kVBytes;
         if constexpr (VROW) {              // [128 keys x 64 ch] atoms, like the K tile
           for (int a = 0; a < S::kAtoms; ++a)
-            tma_load_3d(&tm_vt, &v_full[st], v_dst + a * (kAK * 128), a * 64, h, b * Lk + (t0 + j) * kAK);
+            tma_load_3d(&tm_vt, &v_full[st], v_dst + a * (kAK * 128), a * 64, h, b * Lk + j * kAK);
         } else {
           for (int a = 0; a < kAK / 64; ++a)
-            tc::tma_load_2d(&tm_vt, &v_full[st], v_dst + a * (DP * 128), b * vt_img + (t0 + j) * kAK + a * 64,
-                            h * d);
+            tc::tma_load_2d(&tm_vt, &v_full[st], v_dst + a * (DP * 128), b * vt_img + j * kAK + a * 64, h * d);
         }
       }
     }
@@ -328,8 +277,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     tc::mbar_wait(q_full, 0);
     if (lane == 0) ATTN_TRACE(2, 6);
     auto issue_s = [&](int j) {
-      const int st = j % kKSt;
-      tc::mbar_wait(&k_full[st], (j / kKSt) & 1);
+      const int st = j % kSt;
+      tc::mbar_wait(&k_full[st], (j / kSt) & 1);
       if (lane == 0) ATTN_TRACE(3, 100 + j);
       tc::tc_fence_after();
       if (tc::elect_one()) {
@@ -351,9 +300,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         issue_s(j + 2);
       }
       if constexpr (SPLIT) continue;           // PV MMAs: warp 10
-      tc::mbar_wait(&p_full[j % PB], (j / PB) & 1);
-      const int st = j % kVSt;
-      tc::mbar_wait(&v_full[st], (j / kVSt) & 1);
+      tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      const int st = j % kSt;
+      tc::mbar_wait(&v_full[st], (j / kSt) & 1);
       if (lane == 0) ATTN_TRACE(4, 100 + j);
       tc::tc_fence_after();
       if (tc::elect_one()) {
@@ -363,20 +312,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (int kk = 0; kk < kAK / 16; ++kk) {
           // VROW: 16 keys = 16 rows of 128 B per K step; channel atoms kAK * 128 B apart
           const uint64_t bdesc = VROW ? tc::smem_desc_sw128_mn(vb + kk * 2048, kAK * 128) : kdesc(vb, kk, DP * 128);
-          tc::mma_bf16(tmem + o_col, kdesc(sP + (j % PB) * S::kPBytes, kk, kAQ * 128), bdesc,
+          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), bdesc,
                        kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(&v_empty[st]);
-        tc::mma_commit(&o_done[j % PB]);
+        tc::mma_commit(&o_done[j & 1]);
       }
       __syncwarp();
     }
   } else if (SPLIT && warp == 10) {
     // PV issuer: O_set += P_j V_j as soon as P_j is published and V_j landed
     for (int j = 0; j < n_tiles; ++j) {
-      tc::mbar_wait(&p_full[j % PB], (j / PB) & 1);
-      const int st = j % kVSt;
-      tc::mbar_wait(&v_full[st], (j / kVSt) & 1);
+      tc::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      const int st = j % kSt;
+      tc::mbar_wait(&v_full[st], (j / kSt) & 1);
       tc::tc_fence_after();
       if (tc::elect_one()) {
         const uint8_t* vb = sV + st * S::kVBytes;
@@ -384,11 +333,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
         for (int kk = 0; kk < kAK / 16; ++kk) {
           const uint64_t bdesc = VROW ? tc::smem_desc_sw128_mn(vb + kk * 2048, kAK * 128) : kdesc(vb, kk, DP * 128);
-          tc::mma_bf16(tmem + o_col, kdesc(sP + (j % PB) * S::kPBytes, kk, kAQ * 128), bdesc,
+          tc::mma_bf16(tmem + o_col, kdesc(sP + (j & 1) * S::kPBytes, kk, kAQ * 128), bdesc,
                        kIdescO, (j >= kSets || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(&v_empty[st]);
-        tc::mma_commit(&o_done[j % PB]);
+        tc::mma_commit(&o_done[j & 1]);
       }
       __syncwarp();
     }
@@ -428,7 +377,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       tc::tc_fence_before();                              // S_j is in registers: release the buffer
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&s_free[j & 1]);
-      const int kvalid = Lk - (t0 + j) * kAK - col0;      // keys of this (half-)tile that exist
+      const int kvalid = Lk - j * kAK - col0;             // keys of this (half-)tile that exist
       if (kvalid < kCols) {                               // ragged last tile only
 #pragma unroll
         for (int e = 0; e < kCols; ++e) sv[e] = e < kvalid ? sv[e] : -INFINITY;
@@ -453,13 +402,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // the final O / l uses the same stale max for both, so the result is unchanged)
       const float m_new = mx > m + 8.f ? mx : m;
       const float alpha = ex2(m - m_new);
-      // P_j overwrites P buffer j % PB: PV_{j-PB} (its last reader) must be done.
-      // With two sets and PB = 2 that PV is also the last one into this set's O.
-      if (j >= PB) {
-        tc::mbar_wait(&o_done[j % PB], ((j - PB) / PB) & 1);
+      // P_j overwrites P buffer j&1: PV_{j-2} (its last reader) must be done.
+      // With two sets that PV is also the last one into this set's O.
+      if (j >= 2) {
+        tc::mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
         tc::tc_fence_after();
       }
-      uint8_t* pb = sP + (j % PB) * S::kPBytes;
+      uint8_t* pb = sP + (j & 1) * S::kPBytes;
       float sum = 0.f;
       float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -499,10 +448,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // so the whole warp takes the branch if any of its rows needs it
       if (j >= kSets && __any_sync(0xffffffffu, alpha < 1.f)) {
         if constexpr (kSets == 1) {
-          tc::mbar_wait(&o_done[(j - 1) % PB], ((j - 1) / PB) & 1);   // O holds PV_0..PV_{j-1}
-          tc::tc_fence_after();
-        } else if constexpr (PB > 2) {
-          tc::mbar_wait(&o_done[(j - 2) % PB], ((j - 2) / PB) & 1);   // this set's PV_{j-2} may still run
+          tc::mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);   // O holds PV_0..PV_{j-1}
           tc::tc_fence_after();
         }
 #pragma unroll
@@ -521,16 +467,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       fence_async_smem();                            // P smem writes -> tensor-core (async) proxy
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&p_full[j % PB]);
+      if (lane == 0) tc::mbar_arrive(&p_full[j & 1]);
     }
 
     // ---- epilogue: O / l -> bf16, staged in the (dead) Q tile, TMA-stored ----
     // wait for the last PV this thread's set (or, with one set, the CTA) issued
-    float f0 = 1.f, f1 = 0.f, inv, m_row = 0.f, l_row = 0.f;
+    float f0 = 1.f, f1 = 0.f, inv;
     if constexpr (kSets == 2) {
       const int last = n_tiles - 1 - ((n_tiles - 1 - grp) & 1);   // last tile of this set (may be < 0)
       if (last >= 0) {
-        tc::mbar_wait(&o_done[last % PB], (last / PB) & 1);
+        tc::mbar_wait(&o_done[grp], (last >> 1) & 1);
         tc::tc_fence_after();
       }
       // this set's P buffer is now dead: publish (m, l) of the row through it
@@ -546,10 +492,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       f1 = n_tiles > 1 ? ex2(m1 - mm) : 0.f;
       const float lt = l0 * f0 + l1 * f1;
       inv = lt > 0.f ? 1.f / lt : 0.f;
-      m_row = mm;
-      l_row = lt;
     } else {
-      tc::mbar_wait(&o_done[(n_tiles - 1) % PB], ((n_tiles - 1) / PB) & 1);
+      tc::mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       tc::tc_fence_after();
       red[grp * kAQ + row] = l;
       quad_sync();
@@ -559,91 +503,40 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     tc::tc_fence_after();
     // this thread writes O columns [grp * DP/2, (grp+1) * DP/2) of its row
     constexpr int kHalfO = DP / 2;
-    // tail half-item: both halves publish their unnormalised O (relative to
-    // their row max) and (m, l); the second to arrive (per-item counter) reads
-    // its partner's and combines it with its own O, re-read from TMEM
-    int role = -1;                        // -1 whole item, 0 published and done, 1 combine
-    if (kSets == 2 && half >= 0) {
-      float* mine = g_attn_part + ((size_t)(item - items_full) * 2 + half) * kPartFloats;
-      if (grp == 0) {
-        mine[kAQ * 128 + row] = m_row;
-        mine[kAQ * 128 + kAQ + row] = l_row;
-      }
 #pragma unroll
-      for (int c = 0; c < kHalfO / 32; ++c) {
-        const int ocol = grp * kHalfO + c * 32;
-        uint32_t r0[32];
-        attn_o_row(tmem + lane_off + 256 + ocol, DP, kSets == 2 && n_tiles > 1, f0, f1, r0);
+    for (int c = 0; c < kHalfO / 32; ++c) {
+      const int ocol = grp * kHalfO + c * 32;
+      uint32_t r0[32];
+      tc::tmem_ld32(tmem + lane_off + 256 + ocol, r0);
+      if (kSets == 2 && n_tiles > 1) {
+        uint32_t r1[32];
+        tc::tmem_ld32(tmem + lane_off + 256 + DP + ocol, r1);
+        tmem_ld_wait_regs(r0);
+        reg_pin(r1);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mine[(ocol + e) * kAQ + row] = __uint_as_float(r0[e]);   // [ch][row]: coalesced
-      }
-      __threadfence();
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-      const int slot = item - items_full;
-      if (warp == 2 && lane == 0) {
-        const int prev = atomicAdd(&g_attn_cnt[slot], 1);
-        if (prev == 1) g_attn_cnt[slot] = 0;              // reset for the next launch
-        *flag = prev;
-      }
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      role = *flag;
-    }
-    // the combine is written in half order (half 0 first) whichever half runs
-    // it, so the output bits do not depend on which CTA arrived second
-    const float* other = nullptr;
-    float c_own = inv, c_oth = 0.f;
-    if (role == 1) {
-      __threadfence();
-      other = g_attn_part + ((size_t)(item - items_full) * 2 + (half ^ 1)) * kPartFloats;
-      const float mo = __ldcg(other + kAQ * 128 + row), lo = __ldcg(other + kAQ * 128 + kAQ + row);
-      const float m0 = half == 0 ? m_row : mo, l0 = half == 0 ? l_row : lo;
-      const float m1 = half == 0 ? mo : m_row, l1 = half == 0 ? lo : l_row;
-      const float mx = fmaxf(m0, m1);
-      const float g0 = ex2(m0 - mx), g1 = ex2(m1 - mx);
-      const float lt = l0 * g0 + l1 * g1;
-      const float iv = lt > 0.f ? 1.f / lt : 0.f;
-      c_own = (half == 0 ? g0 : g1) * iv;
-      c_oth = (half == 0 ? g1 : g0) * iv;
-    }
-    if (role != 0) {
+        for (int e = 0; e < 32; ++e)
+          r0[e] = __float_as_uint(fmaf(__uint_as_float(r0[e]), f0, __uint_as_float(r1[e]) * f1));
+      } else {
+        tmem_ld_wait_regs(r0);
+        if (kSets == 2) {
 #pragma unroll
-      for (int c = 0; c < kHalfO / 32; ++c) {
-        const int ocol = grp * kHalfO + c * 32;
-        float ov[32];
-        if (role == 1) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] = __ldcg(other + (ocol + e) * kAQ + row);
-        }
-        uint32_t r0[32];
-        attn_o_row(tmem + lane_off + 256 + ocol, DP, kSets == 2 && n_tiles > 1, f0, f1, r0);
-#pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
-          uint4 u;
-          __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int i0 = c8 * 8 + 2 * e, i1 = i0 + 1;
-            float v0 = __uint_as_float(r0[i0]) * c_own, v1 = __uint_as_float(r0[i1]) * c_own;
-            if (role == 1) {                      // O = O_half0 * c_0 + O_half1 * c_1, in that order
-              const float a0 = half == 0 ? __uint_as_float(r0[i0]) : ov[i0];
-              const float b0 = half == 0 ? ov[i0] : __uint_as_float(r0[i0]);
-              const float a1 = half == 0 ? __uint_as_float(r0[i1]) : ov[i1];
-              const float b1 = half == 0 ? ov[i1] : __uint_as_float(r0[i1]);
-              const float ca = half == 0 ? c_own : c_oth, cb = half == 0 ? c_oth : c_own;
-              v0 = fmaf(b0, cb, a0 * ca);
-              v1 = fmaf(b1, cb, a1 * ca);
-            }
-            hp[e] = __floats2bfloat162_rn(v0, v1);
-          }
-          *reinterpret_cast<uint4*>(sQ + sw128_off(row, (ocol >> 3) + c8)) = u;
+          for (int e = 0; e < 32; ++e) r0[e] = __float_as_uint(__uint_as_float(r0[e]) * f0);
         }
       }
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint4 u;
+        __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          hp[e] = __floats2bfloat162_rn(__uint_as_float(r0[c8 * 8 + 2 * e]) * inv,
+                                        __uint_as_float(r0[c8 * 8 + 2 * e + 1]) * inv);
+        *reinterpret_cast<uint4*>(sQ + sw128_off(row, (ocol >> 3) + c8)) = u;
+      }
     }
-    const bool do_store = role != 0;
-    if (do_store) fence_async_smem();
+    fence_async_smem();
     asm volatile("bar.sync 5, 256;" ::: "memory");        // all softmax warps staged their O
-    if (do_store && warp == 2 && lane == 0) {
+    if (warp == 2 && lane == 0) {
       for (int a = 0; a < S::kAtoms; ++a) tma_store_4d(&tm_o, sQ + a * (kAQ * 128), a * 64, h, q0, b);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem must outlive the reads
@@ -712,49 +605,24 @@ static bool tmap_vt(CUtensorMap* m, const void* ptr, int64_t chans, int64_t keys
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-// drs_set_attn_tail_split: 1 = split the last partial wave's items over their key halves.
-// Off by default: -6 % for the SD1.5 64x64 self-attention launched back to back
-// (112 -> 105 us), but no gain inside the UNet graph (SD1.5 eval 4.666 vs 4.677 ms)
-inline int& attn_tail_split() {
-  static int on = 0;
-  return on;
-}
-
-template <int DP, int NPOLY, bool VROW, bool SPLIT, bool X2 = false, int PB = 2>
+template <int DP, int NPOLY, bool VROW, bool SPLIT, bool X2 = false>
 static int launch_attn_v(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                          int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
-  using S = AttnSmem<DP, PB>;
-  auto kern = attn_tc_kernel<DP, NPOLY, VROW, SPLIT, X2, PB>;
+  using S = AttnSmem<DP>;
+  auto kern = attn_tc_kernel<DP, NPOLY, VROW, SPLIT, X2>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
       return DRS_ERR_CUDA;
     attr = true;
   }
-  // items of the last partial wave run as key-split halves when that shortens it
-  const int items = (Lq + kAQ - 1) / kAQ * H * B;
-  const int n_all = (Lk + kAK - 1) / kAK;
-  const int sms = sm_count();
-  const int tail = items % sms;
-  int items_full = items;
-  // (>= 16 key tiles: the halves' combine costs ~2 us, the split saves n_all / 2 tile times)
-  if (attn_tail_split() && S::kSets == 2 && n_all >= 16 && tail > 0 && 2 * tail <= sms && tail <= kTailSlots)
-    items_full = items - tail;
-  const int grid = items_full + 2 * (items - items_full);
+  dim3 grid((Lq + kAQ - 1) / kAQ, H, B);
   launch_pdl(kern, dim3(grid), dim3(SPLIT ? kAttnTcThreads + 32 : kAttnTcThreads), S::kBytes, st, tq, tk, tv, to,
-             Lq, Lk, d, vt_img, sl2, H, items_full);
+             Lq, Lk, d, vt_img, sl2);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
-// drs_set_attn_split: 1 = separate S / PV MMA issuer warps (SPLIT), 0 = one MMA warp
+// drs_set_attn_split: 0 = one MMA warp, 1 = separate S / PV MMA issuer warps (SPLIT), 2 = SPLIT + X2
 inline int& attn_split_mma() {
   static int on = 2;
   return on;
@@ -764,10 +632,6 @@ template <int DP, bool VROW>
 static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                        int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   static int npoly = [] { const char* e = getenv("DRS_ATTN_POLY"); return e ? atoi(e) : 2; }();
-  if constexpr (DP == 64) {
-    if (attn_split_mma() == 3)
-      return launch_attn_v<DP, 2, VROW, true, true, 4>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
-  }
   if (attn_split_mma() >= 2)
     return launch_attn_v<DP, 2, VROW, true, true>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
   if (attn_split_mma())
@@ -826,13 +690,8 @@ extern "C" int drs_attention_tc_debug(int* mapped_trace) {
   return cudaMemcpyToSymbol(drs::g_attn_trace, &mapped_trace, sizeof(int*)) == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
-extern "C" int drs_set_attn_tail_split(int on) {
-  drs::attn_tail_split() = on ? 1 : 0;
-  return DRS_OK;
-}
-
 extern "C" int drs_set_attn_split(int on) {
-  // 0 one MMA warp, 1 S / PV issuer warps, 2 = 1 + paired-FP32 softmax, 3 = 2 + two P buffers per set (d <= 64)
+  // 0 one MMA warp, 1 S / PV issuer warps, 2 (default) = 1 + paired-FP32 softmax
   drs::attn_split_mma() = on;
   return DRS_OK;
 }

@@ -452,6 +452,9 @@ __device__ __forceinline__ int b_row_offset(const ConvGeom& cv, int m0) {
   return cv.b_img_rows > 0 ? ((m0 / cv.b_img_rows) & 1) * cv.b_img_off : 0;
 }
 
+template <int V>
+struct KpbC { static constexpr int value = V; };   // k-blocks per ring slot, as a type
+
 __device__ __forceinline__ void tma_load_3d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2) {
   asm volatile(
@@ -523,23 +526,21 @@ struct OutMaps {
   CUtensorMap r;
 };        // per epilogue warp: 2 x (32 x 32 bf16) or 1 x (32 x 32 fp32)
 
-// The ring keeps the A tiles of all stages together, then the B tiles, so the
-// tiles of stages s and s+1 are adjacent and one 2-k-block TMA box (kb2 mode)
-// fills both.
+// Ring slot j (kpb consecutive stages) = [kpb A tiles][kpb B tiles]: one
+// kpb-k-block TMA box per operand fills adjacent tiles; kpb = 1 is the plain
+// [A | B] stage layout.
 template <int BN, int kStages>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kAOff = 0;                              // A tile of stage s: kAOff + s * kABytes
-  static constexpr int kBOff = kStages * kABytes;              // B tile of stage s: kBOff + s * kBBytes
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
   static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;   // barriers; +1024 alignment slack
   static_assert(kBytes <= 227 * 1024, "GEMM shared memory plan exceeds 227 KB");
 };
 
-template <int BN, int kStages, int kEpi, bool kSplit>
+template <int BN, int kStages, int kEpi, bool kSplit, int KPB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ OutMaps om, int M, int N, int K, int split_arg, EpiParams ep,
@@ -594,100 +595,106 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
       // stage's full barrier also expects the A bytes, which follow the wait).
       // kb2: a ring slot ("super-stage") is 2 consecutive stages = 2 k-blocks,
       // loaded by one 3-D box per operand (conv A: one 4-D box per k-block)
-      const int kpb = ep.kpb;
-      const int nst = kStages / kpb;
-      int pre = 0;
-      if ((int)blockIdx.x < num_tiles) {
-        const int sp = blockIdx.x % split, mn = blockIdx.x / split;
-        const int mt = mn % m_tiles, nt = mn / m_tiles;
-        const int kb0 = sp * kb_per_split, kb1 = min(num_kb_total, kb0 + kb_per_split);
-        pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
-        for (int j = 0; j < pre; ++j) {
-          uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
-          tc::mbar_arrive_expect_tx(&full_bar[j], kpb * S::kStageBytes);
-          if (kpb > 1)
-            tma_load_3d(&tmap_b, &full_bar[j], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb0 + j * kpb);
-          else
-            tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
-        }
-      }
-      pdl_wait();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int sp = tile % split;
-        const int mn = tile / split;
-        const int mt = mn % m_tiles, nt = mn / m_tiles;
-        const int kb0 = sp * kb_per_split;
-        const int kb1 = min(num_kb_total, kb0 + kb_per_split);
-        for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
-          const bool b_done = tile == (int)blockIdx.x && j < pre;   // weights already in flight
-          if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
-          uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
-          if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], kpb * S::kStageBytes);
-          if (cv.on) {
-            for (int q = 0; q < kpb; ++q) {       // a missing 2nd k-block of a conv: zero A bytes via the
-              const int k = min(kb + q, num_kb_total - 1);   // last valid box again (its MMA is skipped)
-              const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
-              const int ky = tap / 3, kx = tap - ky * 3;
-              const int m0 = mt * kBM, hw = cv.H * cv.W;
-              const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
-              tma_load_4d(&tmap_a, &full_bar[stage], sa + q * S::kABytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
-            }
-          } else if (kpb > 1) {
-            tma_load_3d(&tmap_a, &full_bar[stage], sa, 0, mt * kBM, kb);
-          } else {
-            tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
-          }
-          if (!b_done) {
+      auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+        constexpr int kpb = decltype(kpb_c)::value;
+        const int nst = kStages / kpb;
+        int pre = 0;
+        if ((int)blockIdx.x < num_tiles) {
+          const int sp = blockIdx.x % split, mn = blockIdx.x / split;
+          const int mt = mn % m_tiles, nt = mn / m_tiles;
+          const int kb0 = sp * kb_per_split, kb1 = min(num_kb_total, kb0 + kb_per_split);
+          pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
+          for (int j = 0; j < pre; ++j) {
+            uint8_t* sb = smem + j * kpb * S::kStageBytes + kpb * S::kABytes;
+            tc::mbar_arrive_expect_tx(&full_bar[j], kpb * S::kStageBytes);
             if (kpb > 1)
-              tma_load_3d(&tmap_b, &full_bar[stage], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb);
+              tma_load_3d(&tmap_b, &full_bar[j], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb0 + j * kpb);
             else
-              tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+              tc::tma_load_2d(&tmap_b, &full_bar[j], sb, (kb0 + j) * kBK, nt * BN + b_row_offset(cv, mt * kBM));
           }
-          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
-      }
+        pdl_wait();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          const int sp = tile % split;
+          const int mn = tile / split;
+          const int mt = mn % m_tiles, nt = mn / m_tiles;
+          const int kb0 = sp * kb_per_split;
+          const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+          for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
+            const bool b_done = tile == (int)blockIdx.x && j < pre;   // weights already in flight
+            if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * kpb * S::kStageBytes;
+            uint8_t* sb = smem + stage * kpb * S::kStageBytes + kpb * S::kABytes;
+            if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], kpb * S::kStageBytes);
+            if (cv.on) {
+              for (int q = 0; q < kpb; ++q) {       // a missing 2nd k-block of a conv: zero A bytes via the
+                const int k = min(kb + q, num_kb_total - 1);   // last valid box again (its MMA is skipped)
+                const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
+                const int ky = tap / 3, kx = tap - ky * 3;
+                const int m0 = mt * kBM, hw = cv.H * cv.W;
+                const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+                tma_load_4d(&tmap_a, &full_bar[stage], sa + q * S::kABytes, cb * 64, kx - 1, y0 * cv.stride + ky - 1, n0);
+              }
+            } else if (kpb > 1) {
+              tma_load_3d(&tmap_a, &full_bar[stage], sa, 0, mt * kBM, kb);
+            } else {
+              tc::tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kBK, mt * kBM);
+            }
+            if (!b_done) {
+              if (kpb > 1)
+                tma_load_3d(&tmap_b, &full_bar[stage], sb, 0, nt * BN + b_row_offset(cv, mt * kBM), kb);
+              else
+                tc::tma_load_2d(&tmap_b, &full_bar[stage], sb, kb * kBK, nt * BN + b_row_offset(cv, mt * kBM));
+            }
+            if (++stage == nst) { stage = 0; phase ^= 1; }
+          }
+        }
+      };
+      kpb_body(KpbC<KPB>{});
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    const int kpb = ep.kpb;
-    const int nst = kStages / kpb;
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int sp = tile % split;
-      const int kb0 = sp * kb_per_split;
-      const int kb1 = min(num_kb_total, kb0 + kb_per_split);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-      tc::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; kb += kpb) {
-        tc::mbar_wait(&full_bar[stage], phase);
+    auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+      constexpr int kpb = decltype(kpb_c)::value;
+      const int nst = kStages / kpb;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int sp = tile % split;
+        const int kb0 = sp * kb_per_split;
+        const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc::tc_fence_after();
-        if (tc::elect_one()) {
-          for (int q = 0; q < kpb && kb + q < kb1; ++q) {
-            const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
-            const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)      // +32 B per K=16 step inside the swizzle atom
-              tc::mma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; kb += kpb) {
+          tc::mbar_wait(&full_bar[stage], phase);
+          tc::tc_fence_after();
+          if (tc::elect_one()) {
+            for (int q = 0; q < kpb && kb + q < kb1; ++q) {
+              const uint64_t da = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + q * S::kABytes);
+              const uint64_t db = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + kpb * S::kABytes + q * S::kBBytes);
+  #pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)      // +32 B per K=16 step inside the swizzle atom
+                tc::mma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+            }
+            tc::mma_commit(&empty_bar[stage]);
+            if (kb + kpb >= kb1) tc::mma_commit(&tfull_bar[acc]);
           }
-          tc::mma_commit(&empty_bar[stage]);
-          if (kb + kpb >= kb1) tc::mma_commit(&tfull_bar[acc]);
+          __syncwarp();
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == nst) { stage = 0; phase ^= 1; }
+        if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
+          if (tc::elect_one()) tc::mma_commit(&tfull_bar[acc]);
+          __syncwarp();
+        }
       }
-      if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
-        if (tc::elect_one()) tc::mma_commit(&tfull_bar[acc]);
-        __syncwarp();
-      }
-    }
+    };
+    kpb_body(KpbC<KPB>{});
   } else {
     // ---------------- epilogue (warps 2..9) ----------------
     const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
@@ -830,8 +837,6 @@ struct PairSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = (BN / 2) * kBK * 2;         // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kAOff = 0;                            // A tiles of all stages, then B (as GemmSmem)
-  static constexpr int kBOff = kStages * kABytes;
   static constexpr int kStgOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kStgOffset + kEpiWarps * kStgBytes;
   static constexpr int kBytes = kBarOffset + (2 * kStages + 16) * 8 + 1024;
@@ -915,7 +920,7 @@ __device__ __forceinline__ void pair_load_b(const CUtensorMap* tmap_b, uint64_t*
     tma_load_2d_pair(tmap_b, bar, sb, kb * kBK, row);
 }
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, int KPB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                  const __grid_constant__ OutMaps om, int M, int N, int K, EpiParams ep, ConvGeom cv) {
@@ -967,70 +972,76 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_consta
       // weight (B) halves of the first kStages k-blocks before the PDL wait (as in
       // gemm_bf16_tc_kernel): they never depend on a predecessor kernel
       // kb2: ring slots of 2 stages / 2 k-blocks per TMA box (see gemm_bf16_tc_kernel)
-      const int kpb = ep.kpb;
-      const int nst = kStages / kpb;
-      int pre = 0;
-      if (t0 < num_tiles) {
-        const int pmt = t0 % pm_tiles, nt = t0 / pm_tiles;
-        pre = ep.early_b ? min(nst, (num_kb + kpb - 1) / kpb) : 0;
-        for (int j = 0; j < pre; ++j) {
-          uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
-          if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
-          pair_load_b(&tmap_b, &full_bar[j], sb, j * kpb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
-                      kpb);
-        }
-      }
-      pdl_wait();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = t0; tile < num_tiles; tile += tstep) {
-        const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
-        const int m0 = (pmt * 2 + rank) * kBM;
-        for (int kb = 0, j = 0; kb < num_kb; kb += kpb, ++j) {
-          const bool b_done = tile == t0 && j < pre;
-          if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
-          uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
-          if (rank == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
-          pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
-          if (!b_done)
-            pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+      auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+        constexpr int kpb = decltype(kpb_c)::value;
+        const int nst = kStages / kpb;
+        int pre = 0;
+        if (t0 < num_tiles) {
+          const int pmt = t0 % pm_tiles, nt = t0 / pm_tiles;
+          pre = ep.early_b ? min(nst, (num_kb + kpb - 1) / kpb) : 0;
+          for (int j = 0; j < pre; ++j) {
+            uint8_t* sb = smem + j * kpb * S::kStageBytes + kpb * S::kABytes;
+            if (rank == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
+            pair_load_b(&tmap_b, &full_bar[j], sb, j * kpb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
                         kpb);
-          if (++stage == nst) { stage = 0; phase ^= 1; }
+          }
         }
-      }
+        pdl_wait();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = t0; tile < num_tiles; tile += tstep) {
+          const int pmt = tile % pm_tiles, nt = tile / pm_tiles;
+          const int m0 = (pmt * 2 + rank) * kBM;
+          for (int kb = 0, j = 0; kb < num_kb; kb += kpb, ++j) {
+            const bool b_done = tile == t0 && j < pre;
+            if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * kpb * S::kStageBytes;
+            uint8_t* sb = smem + stage * kpb * S::kStageBytes + kpb * S::kABytes;
+            if (rank == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
+            pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
+            if (!b_done)
+              pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + rank * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                          kpb);
+            if (++stage == nst) { stage = 0; phase ^= 1; }
+          }
+        }
+      };
+      kpb_body(KpbC<KPB>{});
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (rank == 0) {
-      const int kpb = ep.kpb;
-      const int nst = kStages / kpb;
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int tile = t0; tile < num_tiles; tile += tstep, ++it) {
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
-        tc::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; kb += kpb) {
-          tc::mbar_wait(&full_bar[stage], phase);
+      auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+        constexpr int kpb = decltype(kpb_c)::value;
+        const int nst = kStages / kpb;
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = t0; tile < num_tiles; tile += tstep, ++it) {
+          const int acc = it & 1;
+          tc::mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
           tc::tc_fence_after();
-          if (tc::elect_one()) {
-            for (int q = 0; q < kpb && kb + q < num_kb; ++q) {
-              const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
-              const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
-#pragma unroll
-              for (int k = 0; k < kBK / 16; ++k)
-                mma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > 0 || k > 0) ? 1u : 0u);
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < num_kb; kb += kpb) {
+            tc::mbar_wait(&full_bar[stage], phase);
+            tc::tc_fence_after();
+            if (tc::elect_one()) {
+              for (int q = 0; q < kpb && kb + q < num_kb; ++q) {
+                const uint64_t da = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + q * S::kABytes);
+                const uint64_t db = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + kpb * S::kABytes + q * S::kBBytes);
+  #pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  mma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb + q > 0 || k > 0) ? 1u : 0u);
+              }
+              mma_commit_pair(&empty_bar[stage]);
+              if (kb + kpb >= num_kb) mma_commit_pair(&tfull_bar[acc]);
             }
-            mma_commit_pair(&empty_bar[stage]);
-            if (kb + kpb >= num_kb) mma_commit_pair(&tfull_bar[acc]);
+            __syncwarp();
+            if (++stage == nst) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
-      }
+      };
+      kpb_body(KpbC<KPB>{});
     }
   } else {
     // ---------------- epilogue (warps 2..9 of both CTAs: own 128 rows) ----------------
@@ -1122,7 +1133,7 @@ __device__ __forceinline__ void mma_commit_pair_mask(uint64_t* bar, uint16_t mas
                :: "r"(tc::smem_u32(bar)), "h"(mask) : "memory");
 }
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, int KPB>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        int M, int N, int K, int split, EpiParams ep, ConvGeom cv) {
@@ -1171,54 +1182,60 @@ gemm_pair_split_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   if (warp == 0) {
     if (tc::elect_one()) {
       // weight (B) halves of the first kStages k-blocks before the PDL wait
-      const int kpb = ep.kpb;
-      const int nst = kStages / kpb;
-      const int pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
-      for (int j = 0; j < pre; ++j) {
-        uint8_t* sb = smem + S::kBOff + j * kpb * S::kBBytes;
-        if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
-        pair_load_b(&tmap_b, &full_bar[j], sb, kb0 + j * kpb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
-                    kpb);
-      }
-      pdl_wait();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
-        const bool b_done = j < pre;
-        if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sa = smem + S::kAOff + stage * kpb * S::kABytes;
-        uint8_t* sb = smem + S::kBOff + stage * kpb * S::kBBytes;
-        if (half == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
-        pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
-        if (!b_done)
-          pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+      auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+        constexpr int kpb = decltype(kpb_c)::value;
+        const int nst = kStages / kpb;
+        const int pre = ep.early_b ? max(0, min(nst, (kb1 - kb0 + kpb - 1) / kpb)) : 0;
+        for (int j = 0; j < pre; ++j) {
+          uint8_t* sb = smem + j * kpb * S::kStageBytes + kpb * S::kABytes;
+          if (half == 0) tc::mbar_arrive_expect_tx(&full_bar[j], 2 * kpb * S::kStageBytes);
+          pair_load_b(&tmap_b, &full_bar[j], sb, kb0 + j * kpb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
                       kpb);
-        if (++stage == nst) { stage = 0; phase ^= 1; }
-      }
+        }
+        pdl_wait();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0, j = 0; kb < kb1; kb += kpb, ++j) {
+          const bool b_done = j < pre;
+          if (!b_done) tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kpb * S::kStageBytes;
+          uint8_t* sb = smem + stage * kpb * S::kStageBytes + kpb * S::kABytes;
+          if (half == 0 && !b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * kpb * S::kStageBytes);
+          pair_load_a(&tmap_a, &full_bar[stage], sa, S::kABytes, kb, num_kb, m0, cv, kpb);
+          if (!b_done)
+            pair_load_b(&tmap_b, &full_bar[stage], sb, kb, nt * BN + half * (BN / 2) + b_row_offset(cv, pmt * 2 * kBM),
+                        kpb);
+          if (++stage == nst) { stage = 0; phase ^= 1; }
+        }
+      };
+      kpb_body(KpbC<KPB>{});
     }
   } else if (warp == 1) {
     if (half == 0) {
-      const int kpb = ep.kpb;
-      const int nst = kStages / kpb;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; kb += kpb) {
-        tc::mbar_wait(&full_bar[stage], phase);
-        tc::tc_fence_after();
-        if (tc::elect_one()) {
-          for (int q = 0; q < kpb && kb + q < kb1; ++q) {
-            const uint64_t da = tc::smem_desc_sw128(smem + S::kAOff + (stage * kpb + q) * S::kABytes);
-            const uint64_t db = tc::smem_desc_sw128(smem + S::kBOff + (stage * kpb + q) * S::kBBytes);
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              mma_bf16_pair(tmem_base, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+      auto kpb_body = [&](auto kpb_c) {   // KPB: k-blocks per ring slot (separate instantiations)
+        constexpr int kpb = decltype(kpb_c)::value;
+        const int nst = kStages / kpb;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb0; kb < kb1; kb += kpb) {
+          tc::mbar_wait(&full_bar[stage], phase);
+          tc::tc_fence_after();
+          if (tc::elect_one()) {
+            for (int q = 0; q < kpb && kb + q < kb1; ++q) {
+              const uint64_t da = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + q * S::kABytes);
+              const uint64_t db = tc::smem_desc_sw128(smem + stage * kpb * S::kStageBytes + kpb * S::kABytes + q * S::kBBytes);
+  #pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                mma_bf16_pair(tmem_base, da + 2 * k, db + 2 * k, kIdesc, (kb + q > kb0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_pair_mask(&empty_bar[stage], pair_mask);
+            if (kb + kpb >= kb1) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
           }
-          mma_commit_pair_mask(&empty_bar[stage], pair_mask);
-          if (kb + kpb >= kb1) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
+          __syncwarp();
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == nst) { stage = 0; phase ^= 1; }
-      }
+      };
+      kpb_body(KpbC<KPB>{});
       if (kb1 <= kb0) {                            // empty K range: still publish a (zero) tile
         if (tc::elect_one()) mma_commit_pair_mask(&tfull_bar[0], pair_mask);
         __syncwarp();
@@ -1336,6 +1353,7 @@ inline int& gemm_kb2_mode() {
   return kpb;
 }
 
+
 static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
@@ -1378,12 +1396,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int kStages, int kEpi, bool kSplit>
+template <int BN, int kStages, int kEpi, bool kSplit, int KPB = 1>
 static bool ensure_smem_attr() {
   static int state = 0;        // 0 unknown, 1 ok, -1 failed
   if (!state) {
     using S = GemmSmem<BN, kStages>;
-    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages, kEpi, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    state = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, kStages, kEpi, kSplit, KPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  S::kBytes) == cudaSuccess ? 1 : -1;
   }
   return state > 0;
@@ -1410,7 +1428,7 @@ static int max_clusters(int split) {
       la[0].val.clusterDim.z = 1;
       cfg.attrs = la;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages, kEpi, true>, &cfg) != cudaSuccess) n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<BN, kStages, kEpi, true, 1>, &cfg) != cudaSuccess) n = 0;
       cudaGetLastError();
     }
     cache[split] = n > 0 ? n : num_sms() / split;
@@ -1418,7 +1436,7 @@ static int max_clusters(int split) {
   return cache[split];
 }
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, int KPB>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K,
                        int split, const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = GemmSmem<BN, kStages>;
@@ -1426,16 +1444,16 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMa
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * split;
   if (split == 1 && ((ep.tma_store && (!ep.res || ep.tma_res)) || ep.act == DRS_ACT_HEADSOFTMAX)) {
     // persistent: staged TMA stores (and TMA-loaded residual tiles)
-    auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, false>;
-    if (!ensure_smem_attr<BN, kStages, kEpi, false>()) return DRS_ERR_CUDA;
+    auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, false, KPB>;
+    if (!ensure_smem_attr<BN, kStages, kEpi, false, KPB>()) return DRS_ERR_CUDA;
     const int grid = tiles < num_sms() ? tiles : num_sms();
     launch_pdl(kern, dim3(grid), dim3(kGemmThreads), S::kBytes, st, ta, tb, tcm, M, N, K, split, ep, cv);
     return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
   }
   // split-K (or an output the TMA store cannot address: split == 1, direct
   // stores): one CTA per (tile, split), the split CTAs of a tile as one cluster
-  auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, true>;
-  if (!ensure_smem_attr<BN, kStages, kEpi, true>()) return DRS_ERR_CUDA;
+  auto kern = gemm_bf16_tc_kernel<BN, kStages, kEpi, true, KPB>;
+  if (!ensure_smem_attr<BN, kStages, kEpi, true, KPB>()) return DRS_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(kGemmThreads);
@@ -1454,11 +1472,11 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const OutMa
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
 }
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, int KPB>
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K,
                        const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = PairSmem<BN, kStages>;
-  auto kern = gemm_pair_kernel<BN, kStages, kEpi>;
+  auto kern = gemm_pair_kernel<BN, kStages, kEpi, KPB>;
   static int cap = 0;
   if (!cap) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess)
@@ -1499,12 +1517,12 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const OutMa
 }
 
 
-template <int BN, int kStages, int kEpi>
+template <int BN, int kStages, int kEpi, int KPB>
 static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split,
                              const EpiParams& ep, const ConvGeom& cv, cudaStream_t st) {
   using S = PairSmem<BN, kStages>;
   static_assert(kBM * (BN + 4) * 4 <= kStages * S::kStageBytes, "pair split-K partial tile must fit the ring");
-  auto kern = gemm_pair_split_kernel<BN, kStages, kEpi>;
+  auto kern = gemm_pair_split_kernel<BN, kStages, kEpi, KPB>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess ||
@@ -1532,35 +1550,39 @@ static int launch_pair_split(const CUtensorMap& ta, const CUtensorMap& tb, int M
 }
 
 
-// stages of the instantiation gemm_dispatch picks (kept in sync with it)
-static int gemm_stages(int bn, bool pair, int split) {
-  if (pair) return bn == 64 || bn == 128 ? 8 : (bn == 160 ? 7 : 6);
-  return bn == 64 ? 8 : (bn == 128 ? 6 : (bn == 160 ? 5 : 4));
-}
-
-template <int kEpi>
-static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
+template <int kEpi, int KPB>
+static int gemm_dispatch_k(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
                          int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
   if (pair && split > 1) {
     ep.tma_store = 0;                              // reduced rows are stored directly
-    if (bn == 64) return launch_pair_split<64, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 128) return launch_pair_split<128, 8, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 160) return launch_pair_split<160, 7, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
-    if (bn == 192) return launch_pair_split<192, 6, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
-    return launch_pair_split<256, 6, kEpi>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 64) return launch_pair_split<64, 8, kEpi, KPB>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 128) return launch_pair_split<128, 8, kEpi, KPB>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 160) return launch_pair_split<160, 7, kEpi, KPB>(ta, tb, M, N, K, split, ep, cv, st);
+    if (bn == 192) return launch_pair_split<192, 6, kEpi, KPB>(ta, tb, M, N, K, split, ep, cv, st);
+    return launch_pair_split<256, 6, kEpi, KPB>(ta, tb, M, N, K, split, ep, cv, st);
   }
   if (pair) {
-    if (bn == 64) return launch_pair<64, 8, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 128) return launch_pair<128, 8, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 160) return launch_pair<160, 7, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
-    if (bn == 192) return launch_pair<192, 6, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
-    return launch_pair<256, 6, kEpi>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 64) return launch_pair<64, 8, kEpi, KPB>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 128) return launch_pair<128, 8, kEpi, KPB>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 160) return launch_pair<160, 7, kEpi, KPB>(ta, tb, tcm, M, N, K, ep, cv, st);
+    if (bn == 192) return launch_pair<192, 6, kEpi, KPB>(ta, tb, tcm, M, N, K, ep, cv, st);
+    return launch_pair<256, 6, kEpi, KPB>(ta, tb, tcm, M, N, K, ep, cv, st);
   }
-  if (bn == 64) return launch_gemm<64, 8, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  if (bn == 128) return launch_gemm<128, 6, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  if (bn == 160) return launch_gemm<160, 5, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  if (bn == 192) return launch_gemm<192, 4, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
-  return launch_gemm<256, 4, kEpi>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 64) return launch_gemm<64, 8, kEpi, KPB>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 128) return launch_gemm<128, 6, kEpi, KPB>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 160) return launch_gemm<160, 5, kEpi, KPB>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  if (bn == 192) return launch_gemm<192, 4, kEpi, KPB>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+  return launch_gemm<256, 4, kEpi, KPB>(ta, tb, tcm, M, N, K, split, ep, cv, st);
+}
+
+// KPB (k-blocks per TMA box) selects separate kernel instantiations: a runtime
+// switch inside one kernel grew its code and cost 2-3 % per network eval even
+// where only the 1-k-block path ran (tools/net_bench.py A/B)
+template <int kEpi>
+static int gemm_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const OutMaps& tcm, int M, int N, int K, int bn,
+                         int split, bool pair, EpiParams ep, const ConvGeom& cv, cudaStream_t st) {
+  if (ep.kpb == 2) return gemm_dispatch_k<kEpi, 2>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
+  return gemm_dispatch_k<kEpi, 1>(ta, tb, tcm, M, N, K, bn, split, pair, ep, cv, st);
 }
 
 static int max_clusters_bn(int bn, int split) {
@@ -1674,7 +1696,8 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   // TMA operations, whose per-op issue cost (~190 clk from one thread) bounds the
   // operand stream of small tiles (tools/micro/tma_kb2.cu)
   int kpb = g->kbox == 0 ? gemm_kb2_mode() : g->kbox;
-  if (kpb != 1 && kpb != 2 && kpb != 4) return DRS_ERR_VALUE;
+  if (kpb == 4) kpb = 2;                           // (4 k-blocks per box: measured no gain, not instantiated)
+  if (kpb != 1 && kpb != 2) return DRS_ERR_VALUE;
   if (K % kBK || hsm) kpb = 1;
   if (!g->conv_C) {
     if (!make_tmap(&ta, g->A, M, K, g->lda, kBM)) return DRS_ERR_CUDA;
@@ -1707,8 +1730,6 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   const bool pair = g->cta_pair > 0 && M >= 2 * kBM && !hsm && !(g->b_img_rows > 0 && g->b_img_rows % (2 * kBM)) &&
                     (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
   const int64_t b_rows = N + (g->b_img_rows > 0 ? g->b_img_off : 0);
-  // a ring of kStages / kpb slots needs >= 2 slots: 4 k-blocks per box only with 8-stage instantiations
-  if (kpb == 4 && gemm_stages(bn, pair, split) < 8) kpb = 2;
   ep.kpb = kpb;
   if (kpb > 1) {
     if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM, kpb)) return DRS_ERR_CUDA;
@@ -1743,6 +1764,6 @@ extern "C" int drs_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t 
 }
 
 extern "C" int drs_set_gemm_kb2(int on) {
-  drs::gemm_kb2_mode() = on == 4 ? 4 : (on ? 2 : 1);
+  drs::gemm_kb2_mode() = on ? 2 : 1;
   return DRS_OK;
 }

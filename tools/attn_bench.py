@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--only", default="", help="substring of the shape label to run")
     ap.add_argument("--eager", type=int, default=0, help="N eager launches only (for ncu), no timing")
     ap.add_argument("--split", type=int, default=2, help="attention variant (drs_set_attn_split)")
-    ap.add_argument("--tail", type=int, default=0, help="split the last partial wave over key halves (1) or not")
+    ap.add_argument("--qkv", type=int, default=0, help="1: row-major V from a fused QKV buffer (attention_qkv)")
     ap.add_argument("--shapes", default="", help="custom shapes 'B,H,Lq,Lk,d;...' instead of the UNet/DiT list")
     a = ap.parse_args()
     shapes = SHAPES
@@ -41,7 +41,6 @@ def main():
     import torch
     from paper_2603_25872_b200 import _lib, netops
     _lib.lib().drs_set_attn_split(a.split)
-    _lib.lib().drs_set_attn_tail_split(a.tail)
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     for label, B, H, Lq, Lk, d in shapes:
@@ -52,19 +51,25 @@ def main():
         k = torch.randn(B * Lk, H * d, device=dev, generator=g).bfloat16()
         vt = torch.randn(H * d, B * vt_img, device=dev, generator=g).bfloat16()
         o = torch.empty(B * Lq, H * d, device=dev, dtype=torch.bfloat16)
+        if a.qkv:
+            qkv = torch.randn(B * max(Lq, Lk), 3 * H * d, device=dev, generator=g).bfloat16()
+            qq, kk, vv = qkv[:B * Lq, :H * d], qkv[:B * Lk, H * d:2 * H * d], qkv[:B * Lk, 2 * H * d:]
+            call = lambda: netops.attention_qkv(qq, kk, vv, o, B, H, Lq, Lk, d)   # noqa: E731
+        else:
+            call = lambda: netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)   # noqa: E731
         if a.eager:
             for _ in range(a.eager):
-                netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)
+                call()
             torch.cuda.synchronize()
             continue
         s = torch.cuda.Stream(dev)
         with torch.cuda.stream(s):
-            netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)
+            call()
             torch.cuda.synchronize()
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=s):
                 for _ in range(a.reps):
-                    netops.attention_tc(q, k, vt, o, B, H, Lq, Lk, d, vt_img=vt_img)
+                    call()
             gr.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -9,8 +9,8 @@ for B,H,L,Lk,d in [(2,8,4096,4096,40),(2,16,256,256,72),(1,5,300,333,64),(2,8,10
     vimg = (Lk+7)//8*8
     vt = torch.randn(H*d, B*vimg, device=dev, generator=g).bfloat16()
     outs = []
-    for m in (1, 2, 3, 12):
-        _lib.lib().drs_set_attn_split(m % 10); _lib.lib().drs_set_attn_tail_split(1 if m < 10 else 0)
+    for m in (0, 1, 2):
+        _lib.lib().drs_set_attn_split(m)
         o = torch.empty(B*L, H*d, device=dev, dtype=torch.bfloat16)
         netops.attention_tc(q, k, vt, o, B, H, L, Lk, d, vt_img=vimg); torch.cuda.synchronize()
         outs.append(o.float())
@@ -18,5 +18,5 @@ for B,H,L,Lk,d in [(2,8,4096,4096,40),(2,16,256,256,72),(1,5,300,333,64),(2,8,10
     vf = vt.float().view(H, d, B, vimg)[..., :Lk].permute(2, 0, 3, 1)
     ref = torch.softmax(qf @ kf.transpose(-1, -2) / d**0.5, -1) @ vf
     ref = ref.transpose(1, 2).reshape(B*L, H*d)
-    for m, o in zip((1, 2, 3, 12), outs):
+    for m, o in zip((0, 1, 2), outs):
         print(B,H,L,Lk,d,'mode',m,'rel', ((o-ref).norm()/ref.norm()).item(), 'maxdiff vs mode1', (o-outs[0]).abs().max().item())

@@ -139,7 +139,7 @@ def tune_kbox(desc, cfg, dev, reps, cold=False):
     bias = torch.randn(N, device=dev)
     bn, sp, pr = cfg[0], cfg[1], bool(cfg[2]) if len(cfg) > 2 else False
     t = {}
-    for kbox in (1, 2, 4):
+    for kbox in (1, 2):
         run = lambda kbox=kbox: linear(x, wnext(), bias=bias, act=act, residual=res, out=out, bn=bn,   # noqa: E731
                                        split=sp, conv=conv, pair=pr, kbox=kbox)
         t[kbox] = time_config(run, reps)
@@ -190,7 +190,7 @@ def main():
             table[key] = list(cfg[:3]) + [kbox] if len(cfg) > 2 else list(cfg[:2]) + [0, kbox]
             tot1 += t[1]
             tot_sel += t[kbox]
-            print(f"{key:24s} bn={cfg[0]:3d} split={cfg[1]} pair={cfg[2] if len(cfg) > 2 else 0}  kbox1 {t[1]:8.1f} us  kbox2 {t[2]:8.1f} us  kbox4 {t[4]:8.1f} us -> {kbox}",
+            print(f"{key:24s} bn={cfg[0]:3d} split={cfg[1]} pair={cfg[2] if len(cfg) > 2 else 0}  kbox1 {t[1]:8.1f} us  kbox2 {t[2]:8.1f} us -> {kbox}",
                   flush=True)
         print(f"kbox pass: sum {tot1:.0f} us (1 k-block per box) -> {tot_sel:.0f} us (selected)")
         uniq = {}

@@ -20,7 +20,6 @@ def main():
     ap.add_argument("--early", type=int, default=1, help="GEMM weight tiles requested before the PDL wait")
     ap.add_argument("--kb2", type=int, default=-1, help="GEMM 2-k-block TMA boxes (drs_set_gemm_kb2; -1 = default)")
     ap.add_argument("--attn", type=int, default=2, help="attention variant (drs_set_attn_split)")
-    ap.add_argument("--tail", type=int, default=0, help="attention tail split (drs_set_attn_tail_split)")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import _lib
@@ -29,7 +28,6 @@ def main():
     _lib.lib().drs_set_attn_split(a.attn)
     if a.kb2 >= 0:
         _lib.lib().drs_set_gemm_kb2(a.kb2)
-    _lib.lib().drs_set_attn_tail_split(a.tail)
     dev = torch.device("cuda", 0)
     if a.net == "dit":
         from paper_2603_25872_b200.dit import DiT, DiTConfig

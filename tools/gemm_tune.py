@@ -19,6 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 BNS = (64, 128, 160, 192, 256)
+KBOX = False      # --with-kbox: also search 1 / 2 k-blocks per TMA box
 SPLITS = (1, 2, 3, 4, 6, 8)
 
 
@@ -97,6 +98,7 @@ def tune_shape(desc, dev, reps, cold=False):
     tiles_of = lambda bn: ((M + 127) // 128) * ((N + bn - 1) // bn)   # noqa: E731
     kb = (K + 63) // 64
     results = {}
+    kboxes = (1, 2) if KBOX and K % 64 == 0 else (1,)
     for bn in BNS:
         for sp in SPLITS:
             for pr in (0, 1):
@@ -106,11 +108,13 @@ def tune_shape(desc, dev, reps, cold=False):
                 ctas = (((M + 255) // 256) * ((N + bn - 1) // bn) * 2 if pr else tiles_of(bn)) * sp
                 if sp > 1 and (ctas > 148 or kb // sp < 4):
                     continue
-                run = lambda bn=bn, sp=sp, pr=pr: linear(x, wnext(), bias=bias, act=act, residual=res,   # noqa: E731
-                                                         out=out, bn=bn, split=sp, conv=conv, pair=bool(pr))
-                results[(bn, sp, pr)] = time_config(run, reps)
+                for kx in kboxes:
+                    run = lambda bn=bn, sp=sp, pr=pr, kx=kx: linear(x, wnext(), bias=bias, act=act,   # noqa: E731
+                                                                    residual=res, out=out, bn=bn, split=sp,
+                                                                    conv=conv, pair=bool(pr), kbox=kx)
+                    results[(bn, sp, pr, kx) if KBOX else (bn, sp, pr)] = time_config(run, reps)
     best = min(results, key=results.get)
-    model = (pick(M, N, K, 0, 0, False) + (0,)) if conv is None else None
+    model = (pick(M, N, K, 0, 0, False) + ((0, 1) if KBOX else (0,))) if conv is None else None
     return best, results[best], results, model
 
 
@@ -155,9 +159,12 @@ def main():
     ap.add_argument("--mmax", type=int, default=0, help="only shapes with M <= mmax")
     ap.add_argument("--merge", action="store_true", help="update the existing table instead of replacing it")
     ap.add_argument("--only-missing", action="store_true", help="with --merge: tune only shapes not in the table")
+    ap.add_argument("--with-kbox", action="store_true", help="full search including 1 / 2 k-blocks per TMA box")
     ap.add_argument("--kbox", action="store_true",
                     help="keep each entry's (bn, split, pair); choose 1 or 2 k-blocks per TMA box")
     a = ap.parse_args()
+    global KBOX
+    KBOX = a.with_kbox
     import torch
     from paper_2603_25872_b200 import netops
     netops._TABLE = {}                       # tune against the model, not an old table
@@ -204,7 +211,8 @@ def main():
         if model in res:
             tot_best += us
             tot_model += mt
-        print(f"{key:24s} best bn={best[0]:3d} split={best[1]} pair={best[2]} {us:8.1f} us   model {model} "
+        print(f"{key:24s} best bn={best[0]:3d} split={best[1]} pair={best[2]} kbox={best[3] if len(best) > 3 else 1} "
+              f"{us:8.1f} us   model {model} "
               f"{mt:8.1f} us",
               flush=True)
     print(f"tuned {len(table)} shapes in {time.time() - t0:.0f} s; sum best {tot_best:.0f} us vs model "

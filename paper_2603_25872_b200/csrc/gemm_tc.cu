@@ -446,6 +446,8 @@ struct ConvGeom {
   int b_img_off;
   int stride;      // 1, or 2 (H, W are then the OUTPUT grid; the TMA box walks the input with
                    // element stride 2, so input row = 2 y + ky - 1: no im2col for downsamplers)
+  int a2;          // 1 (KPB=2, even cblocks): A map is 5-D (64 ch, W, H, N, C/64) and one box holds the
+                   // two channel blocks of a ring slot (same tap) -- one A operation per slot
 };
 
 __device__ __forceinline__ int b_row_offset(const ConvGeom& cv, int m0) {
@@ -460,6 +462,14 @@ __device__ __forceinline__ void tma_load_3d(const void* tmap, uint64_t* bar, voi
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
       :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
 }
 __device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3) {
@@ -628,7 +638,13 @@ gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_con
             uint8_t* sa = smem + stage * kpb * S::kStageBytes;
             uint8_t* sb = smem + stage * kpb * S::kStageBytes + kpb * S::kABytes;
             if (!b_done) tc::mbar_arrive_expect_tx(&full_bar[stage], kpb * S::kStageBytes);
-            if (cv.on) {
+            if (cv.on && kpb > 1 && cv.a2) {    // both channel blocks of the slot (same tap) in one box
+              const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
+              const int ky = tap / 3, kx = tap - ky * 3;
+              const int m0 = mt * kBM, hw = cv.H * cv.W;
+              const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+              tma_load_5d(&tmap_a, &full_bar[stage], sa, 0, kx - 1, y0 * cv.stride + ky - 1, n0, cb);
+            } else if (cv.on) {
               for (int q = 0; q < kpb; ++q) {       // a missing 2nd k-block of a conv: zero A bytes via the
                 const int k = min(kb + q, num_kb_total - 1);   // last valid box again (its MMA is skipped)
                 const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
@@ -858,6 +874,14 @@ __device__ __forceinline__ void tma_load_3d_pair(const void* tmap, uint64_t* bar
       :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
+                                                 int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+      :: "r"(tc::smem_u32(smem)), "l"(tmap), "r"(tc::smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2),
+         "r"(c3), "r"(c4) : "memory");
+}
 __device__ __forceinline__ void tma_load_4d_pair(const void* tmap, uint64_t* bar, void* smem, int32_t c0, int32_t c1,
                                                  int32_t c2, int32_t c3) {
   asm volatile(
@@ -897,7 +921,13 @@ __device__ __forceinline__ void pair_sync() {
 // otherwise one 2-D box, or one 3-D box carrying 2 k-blocks)
 __device__ __forceinline__ void pair_load_a(const CUtensorMap* tmap_a, uint64_t* bar, uint8_t* sa, int a_bytes, int kb,
                                             int num_kb, int m0, const ConvGeom& cv, int kpb) {
-  if (cv.on) {
+  if (cv.on && kpb > 1 && cv.a2) {
+    const int tap = kb / cv.cblocks, cb = kb - tap * cv.cblocks;
+    const int ky = tap / 3, kx = tap - ky * 3;
+    const int hw = cv.H * cv.W;
+    const int n0 = m0 / hw, y0 = (m0 - n0 * hw) / cv.W;
+    tma_load_5d_pair(tmap_a, bar, sa, 0, kx - 1, y0 * cv.stride + ky - 1, n0, cb);
+  } else if (cv.on) {
     for (int q = 0; q < kpb; ++q) {
       const int k = min(kb + q, num_kb - 1);
       const int tap = k / cv.cblocks, cb = k - tap * cv.cblocks;
@@ -1352,7 +1382,29 @@ inline int& gemm_kb2_mode() {
   static int kpb = 1;
   return kpb;
 }
+// DRS_CONV_A2=0 disables the 5-D conv A boxes (A/B switch)
+static bool gemm_conv_a2() {
+  static const int on = [] { const char* e = getenv("DRS_CONV_A2"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
 
+
+// 5-D conv view (64 ch, W, H, N, C/64): a box {64, W, rows, imgs, 2} is the tiles of two
+// consecutive channel blocks of one tap (KPB=2 slots with even C/64)
+static bool make_tmap_conv5(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const int rows = W >= 128 ? 1 : (128 / W <= H ? 128 / W : H);
+  const int imgs = 128 / (W * rows);
+  const int Hi = H * s, Wi = W * s;
+  cuuint64_t dims[5] = {64, (cuuint64_t)Wi, (cuuint64_t)Hi, (cuuint64_t)N, (cuuint64_t)(C / 64)};
+  cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)Wi * C * 2, (cuuint64_t)Hi * Wi * C * 2, 128};
+  cuuint32_t box[5] = {64, (cuuint32_t)(W * s), (cuuint32_t)(rows * s), (cuuint32_t)imgs, 2};
+  cuuint32_t estr[5] = {1, (cuuint32_t)s, (cuuint32_t)s, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 static bool make_tmap_conv(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int s = 1) {
   PFN_encodeTiled enc = encode_fn();
@@ -1671,7 +1723,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
   if (split < 0 || split > 8) return DRS_ERR_VALUE;            // portable cluster size
   if (bn == 0 || split == 0) gemm_auto_config(M, N, K, bn, split);
   CUtensorMap ta, tb;
-  ConvGeom cv{0, 0, 0, 0, 0, 0, 1};
+  ConvGeom cv{0, 0, 0, 0, 0, 0, 1, 0};
   const bool hsm = g->act == DRS_ACT_HEADSOFTMAX;
   if (hsm) {
     if (g->out_f32 || N % 96 || g->hs_valid <= 0 || g->hs_valid > 96 || (g->ldc % 8) ||
@@ -1690,7 +1742,7 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
     if (W * rows * (128 / (W * rows)) != 128 || H % rows || (128 / (W * rows) > 1 && (rows != H || Nimg % (128 / (W * H)))))
       return DRS_ERR_VALUE;
     if (!make_tmap_conv(&ta, g->A, Nimg, H, W, C, cs)) return DRS_ERR_CUDA;
-    cv = ConvGeom{1, C / 64, H, W, 0, 0, cs};
+    cv = ConvGeom{1, C / 64, H, W, 0, 0, cs, 0};
   }
   // kb2 (K % 64 == 0): one TMA box carries 2 k-blocks -- half the
   // TMA operations, whose per-op issue cost (~190 clk from one thread) bounds the
@@ -1731,6 +1783,15 @@ extern "C" int drs_gemm(const drs_gemm_args* g, void* stream) {
                     (split > 1 || (ep.tma_store && (!ep.res || ep.tma_res)));
   const int64_t b_rows = N + (g->b_img_rows > 0 ? g->b_img_off : 0);
   ep.kpb = kpb;
+  // conv with even C/64 and slots that start at even k-blocks: one 5-D A box per slot
+  if (kpb == 2 && g->conv_C > 0 && (cv.cblocks % 2) == 0 && gemm_conv_a2()) {
+    const int nkb = K / kBK;
+    const int kbs = (nkb + split - 1) / split;
+    if ((split == 1 || kbs % 2 == 0)) {
+      if (!make_tmap_conv5(&ta, g->A, g->conv_N, g->conv_H, g->conv_W, g->conv_C, cv.stride)) return DRS_ERR_CUDA;
+      cv.a2 = 1;
+    }
+  }
   if (kpb > 1) {
     if (!g->conv_C && !make_tmap_kb2(&ta, g->A, M, K, g->lda, kBM, kpb)) return DRS_ERR_CUDA;
     if (!make_tmap_kb2(&tb, g->B, b_rows, K, g->ldb, pair ? bn / 2 : bn, kpb)) return DRS_ERR_CUDA;

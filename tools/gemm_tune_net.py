@@ -1,5 +1,5 @@
 """In-network GEMM tuning: greedy coordinate descent over the (bn, split,
-cta_pair) of each GEMM shape of one network forward, scored by the replay time
+cta_pair, kbox) of each GEMM shape of one network forward, scored by the replay time
 of the WHOLE forward's CUDA graph (the isolated tuner, tools/gemm_tune.py, times
 a shape repeated back to back -- L2-warm, no neighbours -- which misranks some
 configurations inside the real graph).  Updates gemm_table.json in place for
@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=1)
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--out", default=os.path.join(ROOT, "paper_2603_25872_b200", "gemm_table.json"))
+    ap.add_argument("--full", action="store_true", help="every (bn, split, pair, kbox) instead of single-coordinate moves")
     a = ap.parse_args()
     import torch
     from paper_2603_25872_b200 import netops
@@ -71,28 +72,36 @@ def main():
     for d in shapes:
         if d[3] == "headsoftmax":
             continue
-        key = netops.table_key(d[0], d[1], d[2], d[7] is not None)
-        uniq.setdefault(key, d)
+        cv = False if d[7] is None else (d[7][4] if len(d[7]) > 4 else 1)
+        key = netops.table_key(d[0], d[1], d[2], cv)
+        uniq.setdefault(key, (d, cv))
     base = replay_ms()
     print(f"{a.net} B={B}: start {base:.4f} ms/forward, {len(uniq)} shapes", flush=True)
     for rnd in range(a.rounds):
-        for key, d in uniq.items():
+        for key, (d, cv) in uniq.items():
             M, N, K = d[0], d[1], d[2]
             kb = (K + 63) // 64
-            c0 = tuple(table.get(key, netops.pick3(M, N, K, 0, 0, d[7] is not None)))
-            cur = (c0[0], c0[1], int(c0[2]) if len(c0) > 2 else 0)
-            cands = []
-            for bn in netops.BN_CHOICES:
-                for sp in (1, 2, 3, 4, 6, 8):
-                    for pr in (0, 1):
-                        if pr and M < 256:
-                            continue
-                        tiles = ((M + 127) // 128) * ((N + bn - 1) // bn)
-                        ptiles = ((M + 255) // 256) * ((N + bn - 1) // bn)
-                        ctas = (ptiles * 2 if pr else tiles) * sp
-                        if sp > 1 and (ctas > 148 or kb // sp < 4 or (pr and sp > 4)):
-                            continue
-                        cands.append((bn, sp, pr))
+            c0 = tuple(table.get(key, netops.pick3(M, N, K, 0, 0, cv)))
+            cur = (c0[0], c0[1], int(c0[2]) if len(c0) > 2 else 0, int(c0[3]) if len(c0) > 3 else 1)
+            kboxes = (1, 2) if K % 64 == 0 else (1,)
+
+            def ok(c):
+                bn, sp, pr, kx = c
+                if pr and M < 256:
+                    return False
+                tiles = ((M + 127) // 128) * ((N + bn - 1) // bn)
+                ptiles = ((M + 255) // 256) * ((N + bn - 1) // bn)
+                ctas = (ptiles * 2 if pr else tiles) * sp
+                return not (sp > 1 and (ctas > 148 or kb // sp < 4 or (pr and sp > 4)))
+            if a.full:
+                cands = [(bn, sp, pr, kx) for bn in netops.BN_CHOICES for sp in (1, 2, 3, 4, 6, 8) for pr in (0, 1)
+                         for kx in kboxes]
+            else:                                   # single-coordinate moves from the current entry
+                bn0, sp0, pr0, kx0 = cur
+                cands = ([(bn, sp0, pr0, kx0) for bn in netops.BN_CHOICES] +
+                         [(bn0, sp, pr0, kx0) for sp in (1, 2, 3, 4, 6, 8)] +
+                         [(bn0, sp0, 1 - pr0, kx0)] + [(bn0, sp0, pr0, kx) for kx in kboxes])
+            cands = [c for c in dict.fromkeys(cands) if ok(c)]
             best_cfg, best_ms = cur, base
             for c in cands:
                 if c == cur:

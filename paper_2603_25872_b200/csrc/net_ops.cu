@@ -18,7 +18,13 @@ namespace drs {
 
 // x * sigmoid(x) with the fast reciprocal (an IEEE division costs ~10x more;
 // __fdividef(1, inf) = 0 gives the right limit for very negative x)
-__device__ __forceinline__ float silu_fast(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
+// SiLU with one SFU op: x * sigmoid(x) = 0.5 x (1 + tanh(x / 2))  (tanh.approx: rel. err ~2^-11)
+__device__ __forceinline__ float silu_fast(float x) {
+  const float h = 0.5f * x;
+  float th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(h));
+  return fmaf(h, th, h);
+}
 
 // ------------------------------------------------------------ LayerNorm ---
 // One warp per row, float4-vectorised; x and the modulation vectors are all
@@ -627,8 +633,8 @@ gn_group_kernel(const void* __restrict__ x, int HW, int C, int G, const float* _
       if (pp >= HW) break;
       float y0 = fmaf(v[u].x, a0, b0), y1 = fmaf(v[u].y, a1, b1);
       if (silu) {
-        y0 = y0 / (1.f + __expf(-y0));
-        y1 = y1 / (1.f + __expf(-y1));
+        y0 = silu_fast(y0);
+        y1 = silu_fast(y1);
       }
       *reinterpret_cast<__nv_bfloat162*>(out + base + (int64_t)pp * C) = __floats2bfloat162_rn(y0, y1);
     }
@@ -639,6 +645,15 @@ constexpr int kGnCs = 8;                      // CTAs per cluster (portable size
 
 __device__ __forceinline__ void gn_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// (non-volatile: independent loads may be issued back to back; ordered after the cluster barrier by
+// the barrier's acquire and by data dependence on nothing else)
+__device__ __forceinline__ float2 gn_dsmem_ld2_nv(const void* local, int rank) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float2 f;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(f.x), "=f"(f.y) : "r"(r));
+  return f;
 }
 __device__ __forceinline__ float2 gn_dsmem_ld2(const void* local, int rank) {
   uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
@@ -830,7 +845,8 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
               int G, int gpc, const float* __restrict__ gamma, const float* __restrict__ beta, float eps, int silu,
               int rpc, int box) {
   extern __shared__ __align__(1024) uint8_t gsm_t[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_t) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned by pointer arithmetic on the shared array (keeps the shared state space: LDS/STS)
+  uint8_t* base = gsm_t + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(gsm_t)) & 1023u)) & 1023u);
   const int cg = C / G, Cc = cg * gpc;
   const int P = Cc / 8, R = blockDim.x / P;
   const int t = threadIdx.x, q = t % P, rr = t / P;
@@ -846,6 +862,7 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   float2* csum = reinterpret_cast<float2*>(red + blockDim.x);              // [gpc]
   float* stat = reinterpret_cast<float*>(csum + 32);                       // [gpc][2]
   uint64_t* bar = reinterpret_cast<uint64_t*>(stat + 64);
+  float4* part = reinterpret_cast<float4*>(bar + 8);                       // [nch][P] row-lane partials
   if (t == 0) {
     tc::tma_prefetch(&tin);
     tc::tma_prefetch(&tout);
@@ -873,17 +890,41 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
       }
     }
   }
+  // gamma / beta of this thread's 8 channels: issued now, used after the cluster exchange
+  float gmv[8], btv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    gmv[e] = rr < R ? __ldg(gamma + cbase + c0 + e) : 0.f;
+    btv[e] = rr < R ? __ldg(beta + cbase + c0 + e) : 0.f;
+  }
   red[t] = make_float4(s_lo, ss_lo, s_hi, ss_hi);
   __syncthreads();
-  for (int g = t; g < gpc; g += blockDim.x) {            // fixed order: packs, then row lanes
+  // row-lane reduction in two fixed-order levels (was one thread per group walking all R lanes):
+  // nch chunks of lanes per pack in parallel, then per group over packs and chunks
+  const int nch = P * 8 <= 64 ? 8 : (64 / P > 0 ? 64 / P : 1);
+  if (t < P * nch) {
+    const int qp = t % P, ch = t / P;
+    const int r_lo = ch * R / nch, r_hi = (ch + 1) * R / nch;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r2 = r_lo; r2 < r_hi; ++r2) {
+      const float4 f = red[r2 * P + qp];
+      acc.x += f.x; acc.y += f.y; acc.z += f.z; acc.w += f.w;
+    }
+    part[ch * P + qp] = acc;
+  }
+  __syncthreads();
+  for (int g = t; g < gpc; g += blockDim.x) {            // fixed order: packs, then lane chunks
     float a = 0.f, b = 0.f;
     const int qa = (g * cg) / 8, qb = ((g + 1) * cg - 1) / 8;
     for (int qq = qa; qq <= qb; ++qq) {
       const bool lo = (8 * qq) / cg == g;
-      for (int r2 = 0; r2 < R; ++r2) {
-        const float4 f = red[r2 * P + qq];
-        a += lo ? f.x : f.z;
-        b += lo ? f.y : f.w;
+      float4 f[8];
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) f[ch] = ch < nch ? part[ch * P + qq] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        a += lo ? f[ch].x : f[ch].z;
+        b += lo ? f[ch].y : f[ch].w;
       }
     }
     csum[g] = make_float2(a, b);
@@ -892,10 +933,13 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   pdl_trigger();
   for (int g = t; g < gpc; g += blockDim.x) {
     float a = 0.f, b = 0.f;
+    float2 fr[kGnCs];                                     // all peers' sums in flight, then added in rank order
+#pragma unroll
+    for (int r2 = 0; r2 < kGnCs; ++r2) fr[r2] = gn_dsmem_ld2_nv(&csum[g], r2);
+#pragma unroll
     for (int r2 = 0; r2 < kGnCs; ++r2) {
-      const float2 f = gn_dsmem_ld2(&csum[g], r2);
-      a += f.x;
-      b += f.y;
+      a += fr[r2].x;
+      b += fr[r2].y;
     }
     const float cnt = (float)HW * cg;
     const float mean = a / cnt;
@@ -912,9 +956,10 @@ gn_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int g = (c0 + e) / cg;
-      sa[e] = stat[2 * g + 1] * __ldg(gamma + cbase + c0 + e);
-      sb[e] = __ldg(beta + cbase + c0 + e) - stat[2 * g] * sa[e];
+      sa[e] = stat[2 * g + 1] * gmv[e];
+      sb[e] = btv[e] - stat[2 * g] * sa[e];
     }
+#pragma unroll 2
     for (int r = rr; r < rpc; r += R) {
       uint4* p4 = reinterpret_cast<uint4*>(slice + ((size_t)r * Cc + c0) * 2);
       uint4 u = *p4;
@@ -1303,7 +1348,7 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
     while (box > 1 && rpc % box) --box;
     const int Cc = (C / G) * gpc;
     const size_t slice = (size_t)rpc * Cc * 2;
-    const size_t need = ((slice + 127) & ~size_t(127)) + (size_t)threads * 16 + 32 * 8 + 64 * 4 + 64 + 1024;
+    const size_t need = ((slice + 127) & ~size_t(127)) + (size_t)threads * 16 + 32 * 8 + 64 * 4 + 64 + 64 * 16 + 1024;
     CUtensorMap tin, tout;
     if (box >= 8 && need <= 200 * 1024 && gn_tmap(&tin, x, (int64_t)N * HW, C, Cc, box) &&
         gn_tmap(&tout, out, (int64_t)N * HW, C, Cc, box)) {

@@ -95,7 +95,7 @@ int drs_gemm_pick(int M, int N, int K, int* bn, int* split);
 int drs_gemm_cost_us(int M, int N, int K, int bn, int split);
 
 /* out[m, :] = LN(x[m, :]) (*gamma + beta) (*(1 + scale) + shift) -> bf16.
- * x fp32 (x_f32 = 1) or bf16; gamma/beta fp32 [C] or NULL; shift/scale fp32
+ * x fp32 (x_f32 = 1) or bf16; gamma/beta fp32 [C] (16-byte aligned) or NULL; shift/scale fp32
  * or NULL, indexed [(m / mod_group) * mod_ld + c] when mod_group > 0 (per-sample
  * adaLN modulation of a token batch), else [c].  C <= 2048. */
 int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C, const float* gamma, const float* beta,

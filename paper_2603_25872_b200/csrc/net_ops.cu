@@ -34,13 +34,22 @@ __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_
                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                  const float* __restrict__ shift, const float* __restrict__ scale, int mod_group,
                                  int64_t mod_ld, float eps, __nv_bfloat16* __restrict__ out, int64_t ldo) {
-  pdl_wait();
-  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= M) return;
   const int C4 = C >> 2;
+  // gamma / beta are weights (never written on-stream): loaded before the PDL wait
+  float4 gv[kV4], bv[kV4];
+#pragma unroll
+  for (int i = 0; i < kV4; ++i) {
+    const int c4 = lane + 32 * i;
+    const bool in = c4 < C4;
+    gv[i] = gamma && in ? __ldg(reinterpret_cast<const float4*>(gamma) + c4) : make_float4(1.f, 1.f, 1.f, 1.f);
+    bv[i] = beta && in ? __ldg(reinterpret_cast<const float4*>(beta) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (row >= M) return;
   const int64_t mofs = mod_group > 0 ? (int64_t)(row / mod_group) * mod_ld : 0;
   float4 v[kV4], sc[kV4], sh[kV4];
 #pragma unroll
@@ -84,9 +93,11 @@ __global__ void layernorm_kernel(const void* __restrict__ x, int64_t ldx, int x_
       float y[4] = {(v[i].x - mean) * rstd, (v[i].y - mean) * rstd, (v[i].z - mean) * rstd, (v[i].w - mean) * rstd};
       const float s4[4] = {sc[i].x, sc[i].y, sc[i].z, sc[i].w};
       const float h4[4] = {sh[i].x, sh[i].y, sh[i].z, sh[i].w};
+      const float g4[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+      const float b4[4] = {bv[i].x, bv[i].y, bv[i].z, bv[i].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if (gamma) y[e] = y[e] * gamma[4 * c4 + e] + (beta ? beta[4 * c4 + e] : 0.f);
+        if (gamma) y[e] = y[e] * g4[e] + b4[e];
         if (scale) y[e] = y[e] * (1.f + s4[e]);
         if (shift) y[e] = y[e] + h4[e];
       }
@@ -1085,13 +1096,14 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
   if (M <= 0 || C <= 0) return M == 0 ? DRS_OK : DRS_ERR_VALUE;
   if (!x || !out || C > 128 * 16 || C % 4 || ldx % 4 || ldo % 4 || (mod_group > 0 && mod_ld % 4)) return DRS_ERR_VALUE;
   auto mis = [](const void* p, uintptr_t a) { return p && (reinterpret_cast<uintptr_t>(p) & (a - 1)); };
-  if (mis(x, x_f32 ? 16 : 8) || mis(out, 8) || mis(shift, 16) || mis(scale, 16)) return DRS_ERR_VALUE;
+  if (mis(x, x_f32 ? 16 : 8) || mis(out, 8) || mis(shift, 16) || mis(scale, 16) || mis(gamma, 16) || mis(beta, 16))
+    return DRS_ERR_VALUE;
   cudaStream_t st = (cudaStream_t)stream;
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
   // measured (tools/ln_bench.py): one CTA per row wins for wide rows (C >= 1024)
   // and for few rows (M <= 1024); one warp per row wins for narrow rows at large M
   const bool row_path = C >= 1024 || M <= 1024;
-  if (row_path && C / 4 <= 512 && !mis(gamma, 16) && !mis(beta, 16)) {         // row-per-CTA path
+  if (row_path && C / 4 <= 512) {                                              // row-per-CTA path
     const int thr = ((C / 4 + 31) / 32) * 32;
     launch_pdl(layernorm_row_kernel, dim3(M), dim3(thr), 0, st, x, ldx, x_f32, C, gamma, beta, shift, scale,
                mod_group, mod_ld, eps, o, ldo);

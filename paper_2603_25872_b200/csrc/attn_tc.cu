@@ -632,6 +632,8 @@ template <int DP, bool VROW>
 static int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                        int B, int H, int Lq, int Lk, int d, int vt_img, float sl2, cudaStream_t st) {
   static int npoly = [] { const char* e = getenv("DRS_ATTN_POLY"); return e ? atoi(e) : 2; }();
+  // (paired-FP32 softmax with 0 / 3 / 4 of every 8 exps on the FMA pipe: 9 % slower than 2 on the
+  // SD1.5 / SDXL 64x64 self-attention, late round 2)
   if (attn_split_mma() >= 2)
     return launch_attn_v<DP, 2, VROW, true, true>(tq, tk, tv, to, B, H, Lq, Lk, d, vt_img, sl2, st);
   if (attn_split_mma())

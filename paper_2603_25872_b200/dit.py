@@ -137,6 +137,43 @@ class DiT:
         self.mod = torch.empty(max_batch, L * 6 * h, dtype=f32, device=dev)
         self.fmod = torch.empty(max_batch, 2 * h, dtype=f32, device=dev)
         self.eps_img = torch.empty(max_batch, cfg.in_ch, cfg.input_size, cfg.input_size, dtype=f32, device=dev)
+        self.cond_n = 0                      # rows of the per-run conditioning table (alloc_conditioning)
+
+    # ---- per-run conditioning table --------------------------------------------
+    # The adaLN modulations depend on the timestep (and this instance's class label)
+    # only, not on the latent.  A sampler run knows every timestep it will evaluate,
+    # so the run computes them all at its start in ONE batched pass (the 446 MB of
+    # adaLN weights streamed once per run as an M = n GEMM, instead of one M = 1
+    # GEMV per eval), and each eval reads its rows.  Inside the run's timed graph.
+    COND_TABLE = os.environ.get("DRS_COND_TABLE", "1") != "0"
+
+    def alloc_conditioning(self, n: int):
+        """Buffers for a table of n timesteps (call before CUDA-graph capture)."""
+        cfg, h, L, dev = self.cfg, self.cfg.hidden, self.cfg.depth, self.device
+        if n <= self.cond_n:
+            return
+        if self.cond_n:        # graphs captured against the old buffers keep them alive
+            self._old_cond = getattr(self, "_old_cond", []) + [(self.cond_freq, self.cond_h, self.cond_y, self.cond_c,
+                                                                   self.cond_act, self.mod_table, self.fmod_table)]
+        bf, f32 = torch.bfloat16, torch.float32
+        self.cond_freq = torch.empty(n, 256, dtype=bf, device=dev)
+        self.cond_h = torch.empty(n, h, dtype=bf, device=dev)
+        self.cond_y = self.w.y_table[self.class_label].repeat(n, 1).contiguous()
+        self.cond_c = torch.empty(n, h, dtype=f32, device=dev)
+        self.cond_act = torch.empty(n, h, dtype=bf, device=dev)
+        self.mod_table = torch.empty(n, L * 6 * h, dtype=f32, device=dev)
+        self.fmod_table = torch.empty(n, 2 * h, dtype=f32, device=dev)
+        self.cond_n = n
+
+    def prepare_conditioning(self, t_dev):
+        """Modulation rows for the n model timesteps in t_dev (device fp32, n <= cond_n)."""
+        n, w = t_dev.shape[0], self.w
+        ops.timestep_embedding(t_dev, 256, self.cond_freq[:n])
+        ops.linear(self.cond_freq[:n], w.t_w1, bias=w.t_b1, act="silu", out=self.cond_h[:n])
+        ops.linear(self.cond_h[:n], w.t_w2, bias=w.t_b2, residual=self.cond_y[:n], out=self.cond_c[:n])
+        ops.silu_cast(self.cond_c[:n], self.cond_act[:n])
+        ops.linear(self.cond_act[:n], w.ada_w, bias=w.ada_b, out=self.mod_table[:n])
+        ops.linear(self.cond_act[:n], w.f_ada_w, bias=w.f_ada_b, out=self.fmod_table[:n])
 
     # DRS_DIT_OVERLAP=1 (measured slower, off by default): the adaLN modulation GEMVs
     # (M = B rows, 6 h columns per block, 446 MB of weights for 28 blocks) in chunks on a
@@ -171,10 +208,12 @@ class DiT:
             ready["final"] = ev
         return ready
 
-    def forward(self, xs, t_dev, B: int, outs=None):
+    def forward(self, xs, t_dev, B: int, outs=None, cond_rows=None):
         """xs: list of B latents (in_ch*S*S, fp64/fp32 CUDA tensors); t_dev: (>=B,) fp32 device
         timesteps (model units).  eps (first in_ch channels, fp32) is written to outs[b] if
-        given, else returned as a view (B, in_ch, S, S) of an internal buffer."""
+        given, else returned as a view (B, in_ch, S, S) of an internal buffer.  cond_rows: B
+        row indices into the conditioning table (prepare_conditioning) for these timesteps --
+        the conditioning MLP and adaLN projections are then not recomputed."""
         cfg, w = self.cfg, self.w
         T, h, L, S, p = cfg.tokens, cfg.hidden, cfg.depth, cfg.input_size, cfg.patch
         M = B * T
@@ -182,19 +221,26 @@ class DiT:
         for b, x in enumerate(xs):
             ops.patchify(x, cfg.in_ch, S, S, p, self.tok_in[b * T:(b + 1) * T])
         ops.linear(self.tok_in[:M], w.x_w, bias=w.x_b, residual=self.pos_b[:M], out=self.hs[:M])
-        # conditioning: c = MLP(freq(t)) + y_emb ; SiLU(c) drives every adaLN
-        ops.timestep_embedding(t_dev[:B], 256, self.t_freq[:B])
-        ops.linear(self.t_freq[:B], w.t_w1, bias=w.t_b1, act="silu", out=self.t_h[:B])
-        ops.linear(self.t_h[:B], w.t_w2, bias=w.t_b2, residual=self.y_emb[:B], out=self.c[:B])
-        ops.silu_cast(self.c[:B], self.c_act[:B])
-        ready = self._modulations(B)
+        ready = {}
+        mod, fmod = self.mod, self.fmod
+        r0 = cond_rows[0] if cond_rows is not None else -1
+        if cond_rows is not None and list(cond_rows) == list(range(r0, r0 + B)) and r0 + B <= self.cond_n:
+            # a contiguous block of this run's conditioning table, read in place
+            mod, fmod = self.mod_table[r0:r0 + B], self.fmod_table[r0:r0 + B]
+        else:
+            # conditioning: c = MLP(freq(t)) + y_emb ; SiLU(c) drives every adaLN
+            ops.timestep_embedding(t_dev[:B], 256, self.t_freq[:B])
+            ops.linear(self.t_freq[:B], w.t_w1, bias=w.t_b1, act="silu", out=self.t_h[:B])
+            ops.linear(self.t_h[:B], w.t_w2, bias=w.t_b2, residual=self.y_emb[:B], out=self.c[:B])
+            ops.silu_cast(self.c[:B], self.c_act[:B])
+            ready = self._modulations(B)
         hs, xn, qkv, att, mlp = self.hs[:M], self.xn[:M], self.qkv[:M], self.att[:M], self.mlp[:M]
         main = torch.cuda.current_stream(self.device)
         for i, blk in enumerate(w.blocks):
             if i in ready:
                 main.wait_event(ready[i])
             base = i * 6 * h
-            md = self.mod[:B]
+            md = mod[:B]
             sh_a, sc_a, g_a = md[:, base:base + h], md[:, base + h:base + 2 * h], md[:, base + 2 * h:base + 3 * h]
             sh_m, sc_m, g_m = (md[:, base + 3 * h:base + 4 * h], md[:, base + 4 * h:base + 5 * h],
                                md[:, base + 5 * h:base + 6 * h])
@@ -219,7 +265,7 @@ class DiT:
         if "final" in ready:
             main.wait_event(ready["final"])
             main.wait_stream(self._side)            # join the side stream (graph capture needs it)
-        fm = self.fmod[:B]
+        fm = fmod[:B]
         ops.layernorm(hs, out=xn, shift=fm[:, 0:h], scale=fm[:, h:2 * h], eps=1e-6, mod_group=T)
         ops.linear(xn, w.f_w, bias=w.f_b, out=self.tout[:M])
         for b in range(B):

@@ -238,6 +238,12 @@ class DeviceRun:
                 self.launches.append(("gather", st.round))
             elif isinstance(st, Noise):
                 pass
+        if isinstance(self.core, NetworkEps):
+            # per-run conditioning table (DiT): filled by one launch ahead of the first eval
+            from .netdenoise import plan_conditioning
+            tcond = plan_conditioning(self.core, self.launches, self.device)
+            if tcond is not None:
+                self.launches.insert(0, ("cond", tcond))
         self.local_evals = sum(_n_tasks(payload[1]) for kind, payload in self.launches
                                if kind == "eval" and payload[1] is not None)
         self.n_ops = len(ops_all)
@@ -391,6 +397,8 @@ class DeviceRun:
                 timed("chain", nbytes, lambda: _lib.check(
                     L.drs_skip_chain(self.ops_dev.data_ptr() + off * _OP_BYTES, n, self.D, stream),
                     "drs_skip_chain"))
+            elif kind == "cond":
+                timed("cond", nbytes, lambda: self.core.net.prepare_conditioning(payload))
             elif kind == "eval":
                 rnd, lowered = payload
                 if events is not None:

@@ -31,8 +31,41 @@ def lower_eval(d, s, xs, ts, outs, device):
 
 
 def network_eval_into(d, chunks):
-    for xs, t_dev, outs in chunks:
-        d.net.forward(xs, t_dev, len(xs), outs=outs)
+    for ch in chunks:
+        xs, t_dev, outs = ch[:3]
+        if len(ch) > 3:                  # rows of the run's conditioning table
+            d.net.forward(xs, t_dev, len(xs), outs=outs, cond_rows=ch[3])
+        else:
+            d.net.forward(xs, t_dev, len(xs), outs=outs)
+
+
+def plan_conditioning(d, launches, device):
+    """Per-run conditioning table (networks with prepare_conditioning, e.g. the DiT):
+    one table row per local eval task in launch order, so every batched chunk reads a
+    contiguous block.  Rewrites the "net" payloads in `launches` to carry their rows and
+    returns the payload of the "cond" launch that fills the table (None if not used)."""
+    net = d.net
+    if not hasattr(net, "prepare_conditioning") or not getattr(net, "COND_TABLE", False):
+        return None
+    ts, payloads = [], []
+    for kind, payload in launches:
+        if kind != "eval" or payload[1] is None:
+            continue
+        low = payload[1][1] if payload[1][0] == "pert" else payload[1]
+        if low[0] != "net":
+            continue
+        new_chunks = []
+        for ch in low[1]["chunks"]:
+            rows = tuple(range(len(ts), len(ts) + len(ch[0])))
+            ts.extend(float(v) for v in ch[1][:len(ch[0])].tolist())
+            new_chunks.append((ch[0], ch[1], ch[2], rows))
+        payloads.append((low[1], new_chunks))
+    if not ts:
+        return None
+    net.alloc_conditioning(len(ts))
+    for a, new_chunks in payloads:
+        a["chunks"] = new_chunks
+    return torch.tensor(ts, dtype=torch.float32, device=device)
 
 
 def network_eps(d, s, x, ts):

@@ -1359,6 +1359,7 @@ extern "C" int drs_groupnorm(const void* x, int x_f32, int N, int HW, int C, int
     int box = rpc < 256 ? rpc : 256;
     while (box > 1 && rpc % box) --box;
     const int Cc = (C / G) * gpc;
+    // (~256 threads from the plan; 512 measured slower: 64x64 10.4 -> 13.2 us, SD1.5 eval +2.2 %)
     const size_t slice = (size_t)rpc * Cc * 2;
     const size_t need = ((slice + 127) & ~size_t(127)) + (size_t)threads * 16 + 32 * 8 + 64 * 4 + 64 + 64 * 16 + 1024;
     CUtensorMap tin, tout;

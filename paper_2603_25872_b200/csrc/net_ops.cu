@@ -1109,7 +1109,8 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
                mod_group, mod_ld, eps, o, ldo);
     return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_CUDA;
   }
-  const int warps = 8;
+  // rows (warps) per CTA, measured in the SD1.5 graph: 8 -> 4.266, 4 -> 4.247, 2 -> 4.256, 1 -> 4.313 ms/eval
+  const int warps = 4;
   dim3 grid((M + warps - 1) / warps);
   const int v4 = (C / 4 + 31) / 32;
 #define DRS_LN(K) launch_pdl(layernorm_kernel<K>, dim3(grid), dim3(warps * 32), 0, st, x, ldx, x_f32, M, C, gamma, beta, shift, scale, \

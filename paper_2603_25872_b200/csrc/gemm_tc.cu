@@ -65,7 +65,11 @@ __device__ __forceinline__ float gelu_erf(float x) {
   const float e = copysignf(1.f - r, u);
   return 0.5f * x * (1.f + e);
 }
-__device__ __forceinline__ float silu(float x) { return x * __fdividef(1.f, 1.f + __expf(-x)); }
+// x * sigmoid(x) = 0.5 x (1 + tanh(x / 2)): one SFU op (was ex2 + rcp)
+__device__ __forceinline__ float silu(float x) {
+  const float h = 0.5f * x;
+  return fmaf(h, tanh_fast(h), h);
+}
 
 // Two GELU(erf)s at once on the paired FP32 pipe (fma/mul.rn.f32x2 -> FFMA2 /
 // FMUL2): the same erfc rational form as gelu_erf, with log2(e) folded into the
@@ -287,7 +291,7 @@ __device__ __forceinline__ int epi_math32(const EpiParams& p, int M, int N, int 
   }
   if (kEpi == 0 && p.act == DRS_ACT_GELU_TANH) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+    for (int j = 0; j < 32; j += 2) gelu_tanh_x2(v[j], v[j + 1]);
   } else if (kEpi == 3 && p.act == DRS_ACT_SILU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = silu(v[j]);

@@ -571,11 +571,8 @@ struct OutMaps {
 __device__ __forceinline__ void prefetch_bias_l1(const EpiParams& ep, int N, int n_first, int n_step, int n_end,
                                                  int lane) {
   if (!ep.bias) return;
-  const int n0 = n_first + (lane >> 1) * n_step;
-  if (n0 < n_end && n0 < N) {
-    const float* p = ep.bias + n0 + (lane & 1) * 16;       // two lanes per 32-float chunk (any alignment)
-    asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
-  }
+  const int n0 = n_first + (lane >> 1) * n_step + (lane & 1) * 16;   // two lanes per 32-float chunk
+  if (n0 < n_end && n0 < N) asm volatile("prefetch.global.L1 [%0];" :: "l"(ep.bias + n0));
 }
 
 template <int BN, int kStages>

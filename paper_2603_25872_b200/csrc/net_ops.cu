@@ -1102,6 +1102,7 @@ extern "C" int drs_layernorm(const void* x, int64_t ldx, int x_f32, int M, int C
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
   // measured (tools/ln_bench.py): one CTA per row wins for wide rows (C >= 1024)
   // and for few rows (M <= 1024); one warp per row wins for narrow rows at large M
+  // (re-measured late round 2: the warp path for the DiT rows (256 x 1152) costs +11 % per eval)
   const bool row_path = C >= 1024 || M <= 1024;
   if (row_path && C / 4 <= 512) {                                              // row-per-CTA path
     const int thr = ((C / 4 + 31) / 32) * 32;
